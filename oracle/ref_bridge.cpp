@@ -1,0 +1,339 @@
+// ref_bridge.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// POD (extern "C") bridge over the UNMODIFIED reference library, compiled
+// together with /root/reference/proj/src/*.cpp by oracle/Makefile into
+// oracle/_ref/libsptucker_ref.so.  It lets the Python tests pin the C oracle
+// against the reference itself and lets bench.py time the reference CPU path
+// (`--impl reference`, `cpu_baseline.kind == "reference"`).  Nothing here is
+// linked into the product library.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <vector>
+
+#include "sptucker/common.hpp"
+#include "sptucker/core_optimizer.hpp"
+#include "sptucker/eval.hpp"
+#include "sptucker/factor_optimizer.hpp"
+#include "sptucker/model.hpp"
+#include "sptucker/scheduler.hpp"
+#include "sptucker/sptensor.hpp"
+#include "sptucker/synth.hpp"
+#include "sptucker/trainer.hpp"
+
+using namespace sptucker;
+
+namespace {
+
+// Same code map as the C-ABI (include/sgdt.h) and oracle/sgdt_oracle.h.
+int code_of(const std::exception_ptr& p) {
+  try {
+    std::rethrow_exception(p);
+  } catch (const ConfigError&) {
+    return 2;
+  } catch (const DataError&) {
+    return 3;
+  } catch (const NumericError&) {
+    return 4;
+  } catch (const DomainError&) {
+    return 5;
+  } catch (...) {
+    return 1;
+  }
+}
+
+#define GUARD(...)                           \
+  try {                                      \
+    __VA_ARGS__;                             \
+    return 0;                                \
+  } catch (...) {                            \
+    return code_of(std::current_exception()); \
+  }
+
+struct RefTensor {
+  std::unique_ptr<CooTensor> t;
+};
+struct RefModel {
+  std::unique_ptr<TuckerModel> m;
+};
+struct RefRng {
+  Rng rng;
+  CoreBatchWorkspace core_ws;
+  std::vector<RowBatchWorkspace> row_ws;
+  explicit RefRng(std::uint64_t seed) : rng(seed) {}
+};
+
+Strategy strat_of(int s) {
+  return s == 0 ? Strategy::Serial : (s == 1 ? Strategy::Naive : Strategy::Improved);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_mt_outputs(std::uint64_t seed, std::size_t n, std::uint64_t* out) {
+  GUARD({
+    Rng r(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = r.next_u64();
+  });
+}
+
+int ref_next_below_seq(std::uint64_t seed, std::size_t n, const std::uint64_t* bounds,
+                       std::uint64_t* out) {
+  GUARD({
+    Rng r(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = r.next_below(bounds[i]);
+  });
+}
+
+int ref_gaussian_seq(std::uint64_t seed, std::size_t n, double mean, double sd, double* out) {
+  GUARD({
+    Rng r(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = r.next_gaussian(mean, sd);
+  });
+}
+
+int ref_synth_planted(int order, const std::uint32_t* dims, const std::uint32_t* tJ,
+                      std::uint32_t tR, std::size_t nnz, double noise, double tmean,
+                      double tsd, std::uint64_t seed, std::uint32_t* coords_out,
+                      double* values_out) {
+  GUARD({
+    PlantedSpec spec;
+    spec.shape = Shape(std::vector<std::uint32_t>(dims, dims + order));
+    spec.teacher_ranks = Ranks{std::vector<std::uint32_t>(tJ, tJ + order), tR};
+    spec.nnz = nnz;
+    spec.noise_stddev = noise;
+    spec.teacher_mean = tmean;
+    spec.teacher_stddev = tsd;
+    spec.seed = seed;
+    const CooTensor t = synth_planted(spec);
+    for (std::size_t e = 0; e < t.nnz(); ++e) {
+      const auto c = t.coord(e);
+      std::copy(c.begin(), c.end(), coords_out + e * order);
+      values_out[e] = t.value(e);
+    }
+  });
+}
+
+void* ref_tensor_new(int order, const std::uint32_t* dims, std::size_t nnz,
+                     const std::uint32_t* coords, const double* values, int* rc) {
+  try {
+    auto* h = new RefTensor;
+    h->t = std::make_unique<CooTensor>(
+        Shape(std::vector<std::uint32_t>(dims, dims + order)),
+        std::vector<std::uint32_t>(coords, coords + nnz * order),
+        std::vector<double>(values, values + nnz));
+    *rc = 0;
+    return h;
+  } catch (...) {
+    *rc = code_of(std::current_exception());
+    return nullptr;
+  }
+}
+
+void ref_tensor_free(void* h) { delete static_cast<RefTensor*>(h); }
+
+int ref_tensor_perm(void* h, int mode, std::uint32_t* perm_out, std::uint64_t* offsets_out) {
+  GUARD({
+    const CooTensor& t = *static_cast<RefTensor*>(h)->t;
+    const auto& p = t.mode_perm(mode);
+    std::copy(p.begin(), p.end(), perm_out);
+    const auto& o = t.mode_offsets(mode);
+    std::copy(o.begin(), o.end(), offsets_out);
+  });
+}
+
+// Split into train/test (sptensor.cpp:217-254); outputs sized by the caller:
+// ntest = llround(frac * nnz).
+int ref_train_test_split(void* h, double frac, std::uint64_t seed, std::uint32_t* tr_coords,
+                         double* tr_values, std::uint32_t* te_coords, double* te_values) {
+  GUARD({
+    const CooTensor& t = *static_cast<RefTensor*>(h)->t;
+    auto [tr, te] = train_test_split(t, frac, seed);
+    const std::size_t order = t.order();
+    for (std::size_t e = 0; e < tr.nnz(); ++e) {
+      const auto c = tr.coord(e);
+      std::copy(c.begin(), c.end(), tr_coords + e * order);
+      tr_values[e] = tr.value(e);
+    }
+    for (std::size_t e = 0; e < te.nnz(); ++e) {
+      const auto c = te.coord(e);
+      std::copy(c.begin(), c.end(), te_coords + e * order);
+      te_values[e] = te.value(e);
+    }
+  });
+}
+
+void* ref_model_new(int order, const std::uint32_t* dims, const std::uint32_t* J,
+                    std::uint32_t R, int* rc) {
+  try {
+    auto* h = new RefModel;
+    h->m = std::make_unique<TuckerModel>(Shape(std::vector<std::uint32_t>(dims, dims + order)),
+                                         Ranks{std::vector<std::uint32_t>(J, J + order), R});
+    *rc = 0;
+    return h;
+  } catch (...) {
+    *rc = code_of(std::current_exception());
+    return nullptr;
+  }
+}
+
+void ref_model_free(void* h) { delete static_cast<RefModel*>(h); }
+
+int ref_model_init_gaussian(void* h, double mean, double sd, std::uint64_t seed) {
+  GUARD({
+    TuckerModel& m = *static_cast<RefModel*>(h)->m;
+    m = TuckerModel::init_gaussian(m.shape(), m.ranks(), mean, sd, seed);
+  });
+}
+
+// Copy parameters in (dir=0) or out (dir=1); A and B are arrays of order
+// pointers to row-major fp64 buffers.
+int ref_model_params(void* h, int dir, double* const* A, double* const* B) {
+  GUARD({
+    TuckerModel& m = *static_cast<RefModel*>(h)->m;
+    for (std::size_t n = 0; n < m.order(); ++n) {
+      auto& a = m.factor(n).data();
+      auto& b = m.kruskal(n).data();
+      if (dir == 0) {
+        std::copy(A[n], A[n] + a.size(), a.begin());
+        std::copy(B[n], B[n] + b.size(), b.begin());
+      } else {
+        std::copy(a.begin(), a.end(), A[n]);
+        std::copy(b.begin(), b.end(), B[n]);
+      }
+    }
+    if (dir == 0) m.refresh_core_cache();
+  });
+}
+
+double ref_model_predict(void* h, const std::uint32_t* coord) {
+  const TuckerModel& m = *static_cast<RefModel*>(h)->m;
+  return m.predict(std::span<const std::uint32_t>(coord, m.order()));
+}
+
+void* ref_rng_new(std::uint64_t seed) { return new RefRng(seed); }
+void ref_rng_free(void* h) { delete static_cast<RefRng*>(h); }
+
+int ref_sample_batch(void* rng, void* tensor, std::size_t m, std::uint32_t* out) {
+  GUARD({
+    auto* r = static_cast<RefRng*>(rng);
+    const CooTensor& t = *static_cast<RefTensor*>(tensor)->t;
+    std::vector<std::uint32_t> o;
+    sample_batch(t, m, r->rng, r->core_ws.sample_pool, o);
+    std::copy(o.begin(), o.end(), out);
+  });
+}
+
+// One core epoch; the RNG handle carries the persistent sample pool.
+// batch_out (nullable) receives the last Psi drawn.
+int ref_core_epoch(void* model, void* tensor, void* rng, double lr, double reg,
+                   std::size_t batch_m, int resample, int incremental, int strategy,
+                   std::size_t threads, std::uint32_t* batch_out) {
+  GUARD({
+    auto* r = static_cast<RefRng*>(rng);
+    TuckerModel& m = *static_cast<RefModel*>(model)->m;
+    const CooTensor& t = *static_cast<RefTensor*>(tensor)->t;
+    WorkerPool pool(threads);
+    SchedContext sched{strat_of(strategy), BalancePolicy::Dynamic,
+                       strategy == 0 ? nullptr : &pool};
+    CoreHyper h{lr, reg, batch_m, resample != 0, incremental != 0};
+    update_core_epoch(m, t, h, sched, r->rng, r->core_ws);
+    if (batch_out) std::copy(r->core_ws.batch.begin(), r->core_ws.batch.end(), batch_out);
+  });
+}
+
+int ref_factor_epoch(void* model, void* tensor, void* rng, double lr, double reg,
+                     double row_fraction, int strategy, std::size_t threads,
+                     std::size_t* rows_updated, std::size_t* rows_skipped) {
+  GUARD({
+    auto* r = static_cast<RefRng*>(rng);
+    TuckerModel& m = *static_cast<RefModel*>(model)->m;
+    const CooTensor& t = *static_cast<RefTensor*>(tensor)->t;
+    WorkerPool pool(threads);
+    SchedContext sched{strat_of(strategy), BalancePolicy::Dynamic,
+                       strategy == 0 ? nullptr : &pool};
+    FactorHyper h{lr, reg, row_fraction};
+    const FactorEpochStats st = update_factor_epoch(m, t, h, sched, r->rng, r->row_ws);
+    if (rows_updated) *rows_updated = st.rows_updated;
+    if (rows_skipped) *rows_skipped = st.rows_skipped;
+  });
+}
+
+int ref_rmse_mae(void* model, void* tensor, double* rmse, double* mae) {
+  GUARD({
+    const auto [a, b] =
+        rmse_mae(*static_cast<RefModel*>(model)->m, *static_cast<RefTensor*>(tensor)->t);
+    *rmse = a;
+    *mae = b;
+  });
+}
+
+// train_from_scratch (trainer.cpp:127-139).  metrics: epochs x 6 doubles
+// {core_s, factor_s, train_rmse, train_mae, test_rmse, test_mae}.
+int ref_train_from_scratch(void* train_t, void* test_t, const std::uint32_t* J,
+                           std::uint32_t R, double lr_a, double lr_b, double reg_a,
+                           double reg_b, std::size_t batch_m, double row_fraction,
+                           std::size_t epochs, std::uint64_t seed, double init_mean,
+                           double init_sd, int strategy, std::size_t threads, void* model_out,
+                           double* metrics) {
+  GUARD({
+    const CooTensor& tr = *static_cast<RefTensor*>(train_t)->t;
+    const CooTensor* te = test_t ? static_cast<RefTensor*>(test_t)->t.get() : nullptr;
+    HyperParams h;
+    h.ranks.assign(J, J + tr.order());
+    h.r_core = R;
+    h.lr_a = lr_a;
+    h.lr_b = lr_b;
+    h.reg_a = reg_a;
+    h.reg_b = reg_b;
+    h.batch_m = batch_m;
+    h.row_fraction = row_fraction;
+    h.epochs = epochs;
+    h.seed = seed;
+    h.init_mean = init_mean;
+    h.init_stddev = init_sd;
+    h.strategy = strat_of(strategy);
+    h.threads = threads;
+    auto [m, res] = train_from_scratch(tr, te, h);
+    for (std::size_t e = 0; e < res.metrics.size(); ++e) {
+      const auto& row = res.metrics[e];
+      double* o = metrics + e * 6;
+      o[0] = row.core_s;
+      o[1] = row.factor_s;
+      o[2] = row.train_rmse;
+      o[3] = row.train_mae;
+      o[4] = row.test_rmse;
+      o[5] = row.test_mae;
+    }
+    if (model_out) *static_cast<RefModel*>(model_out)->m = std::move(m);
+  });
+}
+
+// Timed epochs through the reference's own bench path (eval.cpp:201-266):
+// median seconds of (core + factor) per epoch after `warmup` epochs.
+int ref_bench_epoch_seconds(void* train_t, const std::uint32_t* J, std::uint32_t R,
+                            double lr_a, double lr_b, double reg, std::size_t batch_m,
+                            int strategy, std::size_t threads, std::size_t warmup,
+                            std::size_t epochs, std::uint64_t seed, double* seconds) {
+  GUARD({
+    const CooTensor& tr = *static_cast<RefTensor*>(train_t)->t;
+    BenchOptions o;
+    o.epochs = epochs;
+    o.warmup = warmup;
+    o.seed = seed;
+    o.lr_a = lr_a;
+    o.lr_b = lr_b;
+    o.reg = reg;
+    o.batch_m = batch_m;
+    o.strategy = strat_of(strategy);
+    const auto rows = bench_speedup(tr, Ranks{std::vector<std::uint32_t>(J, J + tr.order()), R},
+                                    {threads}, o);
+    *seconds = rows.at(0).seconds_per_epoch;
+  });
+}
+
+}  // extern "C"
