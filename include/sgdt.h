@@ -1,0 +1,170 @@
+/*
+ * sgdt.h -- C-ABI of the B200-native SGD_Tucker training hot path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and POD structs, no
+ * exceptions and no torch types.  The C++ host API that mirrors the reference
+ * (paper_2012_03550_b200/cpp/include/sptucker/*.hpp, namespace sptucker) sits on
+ * top of it, exactly as the reference's per-epoch calls sit on top of its CPU
+ * loops.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ *
+ * Error codes mirror the reference exception taxonomy
+ * (include/sptucker/common.hpp:13-43) and the CLI exit codes
+ * (tools/sptucker_main.cpp:430-445):
+ *   0 OK, 1 internal / CUDA, 2 ConfigError, 3 DataError, 4 NumericError,
+ *   5 DomainError.  sgdt_last_error() returns the message of the last failure
+ *   on the calling thread.
+ *
+ * Conventions (same as the reference): modes are 0-based, coordinate VALUES
+ * are 1-based u32 in entry-major order (CooTensor::coord, sptensor.hpp:80-82),
+ * A^(n) is I_n x J_n row-major, B^(n) is J_n x R row-major, fp64 on the host.
+ * On the device parameters are fp32; the sampler, permutations and shard
+ * assignment are bit-exact with the reference.
+ */
+#ifndef SGDT_H
+#define SGDT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGDT_OK 0
+#define SGDT_ERR_INTERNAL 1
+#define SGDT_ERR_CONFIG 2
+#define SGDT_ERR_DATA 3
+#define SGDT_ERR_NUMERIC 4
+#define SGDT_ERR_DOMAIN 5
+
+#define SGDT_MAX_ORDER 8
+#define SGDT_MAX_RCORE 32
+#define SGDT_MAX_J 64
+
+typedef struct sgdt_session sgdt_session;
+
+/* A CooTensor as the reference holds it (sptensor.hpp:66-107). */
+typedef struct {
+  int order;                          /* N, 2..SGDT_MAX_ORDER */
+  const uint32_t* dims;               /* N */
+  uint64_t nnz;                       /* < 2^32 (sptensor.cpp:87-88) */
+  const uint32_t* coords;             /* nnz*N, 1-based, entry-major */
+  const double* values;               /* nnz */
+  /* Optional: CooTensor::mode_perm(n) for n < N (entry ids bucketed by the
+   * mode-n coordinate, ascending entry id inside a bucket,
+   * sptensor.cpp:102-117).  NULL -> the library computes the same stable
+   * counting sort on the host. */
+  const uint32_t* const* mode_perm;
+} sgdt_tensor_desc;
+
+/* CoreHyper (core_optimizer.hpp:13-19). */
+typedef struct {
+  double lr;
+  double reg;
+  uint64_t batch_m; /* |Psi|; 0 = full training set (no RNG) */
+  int resample_per_mode;
+  int incremental_residual; /* accepted; the device V-identity is exact for both */
+} sgdt_core_hyper;
+
+/* FactorHyper (factor_optimizer.hpp:14-18). */
+typedef struct {
+  double lr;
+  double reg;
+  double row_fraction; /* (0,1]; < 1 draws per-row subsets from the session RNG */
+} sgdt_factor_hyper;
+
+/* CoreEpochStats (core_optimizer.hpp:51-54). */
+typedef struct {
+  uint64_t batch_size;
+  uint64_t effective_workers;
+} sgdt_core_stats;
+
+/* FactorEpochStats (factor_optimizer.hpp:44-48). */
+typedef struct {
+  uint64_t rows_updated;
+  uint64_t rows_skipped;
+  double max_imbalance;
+} sgdt_factor_stats;
+
+/* Per-phase device times of the last epoch run, from CUDA events. */
+typedef struct {
+  float sample_ms;
+  float core_ms;
+  float factor_ms;
+  float factor_mode_ms[SGDT_MAX_ORDER];
+} sgdt_timing;
+
+const char* sgdt_last_error(void);
+const char* sgdt_version(void);
+
+/* Upload a training tensor (and optional test tensor, may be NULL) and size
+ * the device model for ranks J (N entries) and R.  Builds the entry-order
+ * record copy, one mode-sorted record copy per mode (the layout of
+ * CooTensor::mode_perm/mode_offsets) and the nnz-balanced chunk schedule.
+ * Replaces the per-call setup inside update_core_epoch / update_factor_epoch
+ * (core_optimizer.cpp:112-151, factor_optimizer.cpp:101-136).
+ * device < 0 selects the current device. */
+int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test,
+                        const uint32_t* J, uint32_t R, int device, sgdt_session** out);
+void sgdt_session_destroy(sgdt_session* s);
+
+/* The session's CUDA stream (cudaStream_t) -- every kernel runs on it. */
+void* sgdt_session_stream(sgdt_session* s);
+
+/* Model state in/out, fp64 host <-> fp32 device.  A[n] is I_n x J_n, B[n] is
+ * J_n x R (TuckerModel::factor/kruskal, model.hpp:54-58). */
+int sgdt_set_model(sgdt_session* s, const double* const* A, const double* const* B);
+int sgdt_get_model(sgdt_session* s, double* const* A, double* const* B);
+
+/* RNG state crossing the boundary: the 312-word std::mt19937_64 state plus
+ * its position (rng.hpp:46).  The device consumes exactly the outputs the
+ * host Rng would have consumed. */
+int sgdt_set_rng(sgdt_session* s, const uint64_t* mt312, uint32_t pos);
+int sgdt_get_rng(sgdt_session* s, uint64_t* mt312, uint32_t* pos);
+/* Reset the persistent sample pool to iota (CoreBatchWorkspace::sample_pool
+ * sized wrong, sptensor.cpp:260-263). */
+int sgdt_reset_pool(sgdt_session* s);
+
+/* sample_batch (sptensor.cpp:256-270) on the device pool; out (host, m
+ * entries) may be NULL. */
+int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out);
+/* The last Psi drawn by the core phase or sgdt_sample_batch (host copy). */
+int sgdt_last_batch(sgdt_session* s, uint32_t* out, uint64_t* len);
+
+/* update_core_epoch (core_optimizer.cpp:112-257). */
+int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* st);
+/* update_factor_epoch (factor_optimizer.cpp:101-273). */
+int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_stats* st);
+/* `epochs` x (core phase; factor phase) enqueued back to back, one host
+ * synchronisation at the end (the timed part of train(), trainer.cpp:94-107).
+ * A divergence anywhere returns SGDT_ERR_NUMERIC (trainer.cpp:101-103). */
+int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh,
+                    uint64_t epochs);
+
+/* rmse_mae (eval.cpp:15-33) over the training (which=0) or test (which=1)
+ * entries of the session, fp64 accumulation, fixed summation order. */
+int sgdt_eval(sgdt_session* s, int which, double* rmse, double* mae);
+
+/* train() (trainer.cpp:66-125) with the model already set: per epoch core,
+ * factor, finiteness check, train/test RMSE+MAE.  metrics: epochs x 6
+ * {core_s, factor_s, train_rmse, train_mae, test_rmse, test_mae}, core_s and
+ * factor_s measured with CUDA events (RMSE excluded, as in the reference). */
+int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh,
+               uint64_t epochs, double* metrics);
+
+int sgdt_last_timing(sgdt_session* s, sgdt_timing* t);
+
+/* Device next_below over an explicit MT state (test hook for the rejection
+ * path, rng.hpp:20-25): draws n values with bounds[i] sequentially. */
+int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,
+                        uint64_t n, uint64_t* out, uint64_t* mt312_out, uint32_t* pos_out);
+
+/* partition_even (scheduler.cpp:34-46): slice w of count over workers. */
+void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uint64_t* ends);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGDT_H */

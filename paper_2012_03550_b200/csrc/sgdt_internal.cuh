@@ -1,0 +1,153 @@
+// sgdt_internal.cuh -- device session layout shared by the sgdt_*.cu units.
+//
+// HBM layout:
+//   * entry-order record copy: idx[k*nnz + e] (u32, 0-based) for k < N,
+//     val[e] (fp32)  -- Psi gathers of the core phase and train RMSE.
+//   * one mode-sorted copy per mode n, the reference's mode_perm(n) order
+//     (sptensor.cpp:102-117): idx_n[k*nnz + q], val_n[q]; row_ptr[I_n+1];
+//     an nnz-balanced chunk schedule for the factor kernel.
+//   * A^(n) fp32 I_n x J (stride J), B^(n) fp32 J x R, Q^(n) = A^(n) B^(n)
+//     fp32 I_n x RP (RP = R rounded up to a multiple of 4, zero padded, so a
+//     row is float4-gatherable).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sgdt.h"
+
+namespace sgdt {
+
+constexpr int kMaxOrder = SGDT_MAX_ORDER;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// Factor-phase work unit: entries [begin, end) of the mode-sorted copy.
+// piece < 0: the chunk holds whole rows; otherwise it is piece `piece` of a
+// row longer than the chunk size (finalised by the split-row kernel).
+struct Chunk {
+  uint32_t begin;
+  uint32_t end;
+  int32_t piece;
+  uint32_t pad;
+};
+
+// A row split over several chunks: pieces [first, first + count).
+struct SplitRow {
+  uint32_t row;
+  uint32_t first;
+  uint32_t count;
+  uint32_t pad;
+};
+
+struct RecordCopy {
+  uint32_t* idx = nullptr;  // order x nnz
+  float* val = nullptr;     // nnz
+  uint64_t nnz = 0;
+};
+
+struct ModePlan {
+  RecordCopy rec;
+  uint32_t* row_ptr = nullptr;  // I_n + 1
+  Chunk* chunks = nullptr;
+  uint32_t n_chunks = 0;
+  SplitRow* splits = nullptr;
+  uint32_t n_splits = 0;
+  uint32_t n_pieces = 0;
+  uint64_t rows_nonempty = 0;
+  uint64_t rows_empty = 0;
+};
+
+struct Params {
+  int order;
+  uint32_t dims[kMaxOrder];
+  uint32_t J[kMaxOrder];
+  uint32_t R;
+  uint32_t RP;
+  float* A[kMaxOrder];
+  float* B[kMaxOrder];
+  float* Q[kMaxOrder];
+};
+
+struct Session {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int order = 0;
+  uint32_t dims[kMaxOrder] = {};
+  uint32_t J[kMaxOrder] = {};
+  uint32_t R = 0, RP = 0;
+  uint32_t chunk_size = 2048;
+  uint64_t nnz = 0, nnz_test = 0;
+
+  RecordCopy train_rec, test_rec;
+  ModePlan mode[kMaxOrder];
+
+  Params P{};
+  double* piece_partials = nullptr;  // max pieces x RP
+
+  // sampler state
+  uint64_t* mt = nullptr;       // 312 words + position word
+  uint32_t* pool = nullptr;     // nnz, persistent
+  bool pool_valid = false;
+  unsigned long long* head = nullptr;  // nnz stamped list heads
+  uint32_t stamp = 0;
+  uint32_t* draw_j = nullptr;   // m
+  uint32_t* link = nullptr;     // m
+  uint32_t* kprev = nullptr;    // m
+  uint32_t* lprev = nullptr;    // m
+  uint32_t* dval = nullptr;     // m
+  uint32_t* batch = nullptr;    // up to order x m (one Psi per mode when resampling)
+  uint64_t batch_cap = 0;
+  uint64_t last_batch_len = 0;
+  uint32_t* last_batch = nullptr;  // points into batch
+
+  // core scratch (M samples)
+  float* cs_a = nullptr;      // M x Jmax
+  float* cs_c = nullptr;      // M x R
+  float* cs_xhat = nullptr;   // M
+  float* cs_x = nullptr;      // M
+  double* cs_part = nullptr;  // 2 x grid x Jmax
+  uint64_t cs_cap = 0;
+  int core_grid = 0, core_block = 0;
+
+  // eval
+  double* ev_part = nullptr;
+  double* ev_out = nullptr;
+  double* h_ev_out = nullptr;  // pinned
+
+  int* flag = nullptr;    // device numeric-error flag
+  int* h_flag = nullptr;  // pinned mirror
+
+  double* stage = nullptr;  // fp64 staging for model transfer
+  uint64_t stage_cap = 0;
+
+  cudaEvent_t ev[4 + kMaxOrder] = {};
+  sgdt_timing timing{};
+  bool timing_valid = false;
+};
+
+// error plumbing (sgdt_session.cu)
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define SGDT_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return ::sgdt::fail(SGDT_ERR_INTERNAL, std::string(#call) + ": " +             \
+                                                cudaGetErrorString(e_));             \
+  } while (0)
+
+// kernels (launchers return cudaError_t)
+int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch);
+int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, uint64_t m,
+                int per_mode_batches);
+int launch_q_refresh(Session& s, int mode);
+int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h);
+int launch_eval(Session& s, int which, double* rmse, double* mae);
+int launch_cast_model(Session& s, int to_device, int n, double* stage);
+
+}  // namespace sgdt

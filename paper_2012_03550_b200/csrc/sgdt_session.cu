@@ -1,0 +1,707 @@
+// sgdt_session.cu -- the C-ABI (include/sgdt.h): session setup, device
+// layout build, model/RNG transfer, and the per-epoch drivers.
+//
+// The drivers follow the reference's control flow exactly:
+//   core phase   update_core_epoch   (core_optimizer.cpp:112-257)
+//   factor phase update_factor_epoch (factor_optimizer.cpp:101-273)
+//   train loop   train               (trainer.cpp:66-125)
+//   eval         rmse_mae            (eval.cpp:15-33)
+// Every kernel is enqueued on the session stream; the public epoch calls
+// synchronise once at the end to map the device divergence flag onto
+// NumericError, as sgdt_step / all_finite do (core_optimizer.cpp:93-98,
+// trainer.cpp:101-103).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sgdt_internal.cuh"
+
+struct sgdt_session : sgdt::Session {};
+
+namespace sgdt {
+
+namespace {
+thread_local std::string g_error;
+
+__global__ void build_entry_copy_kernel(const uint32_t* __restrict__ coords,
+                                        const double* __restrict__ values, uint64_t nnz,
+                                        int order, uint32_t* idx, float* val) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    for (int k = 0; k < order; ++k) idx[static_cast<uint64_t>(k) * nnz + e] = coords[e * order + k] - 1;
+    val[e] = static_cast<float>(values[e]);
+  }
+}
+
+// Mode-sorted copy: record q of mode n is entry perm[q] (sptensor.cpp:102-117).
+__global__ void gather_mode_copy_kernel(const uint32_t* __restrict__ src_idx,
+                                        const float* __restrict__ src_val,
+                                        const uint32_t* __restrict__ perm, uint64_t nnz, int order,
+                                        uint32_t* idx, float* val) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nnz;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = perm[q];
+    for (int k = 0; k < order; ++k)
+      idx[static_cast<uint64_t>(k) * nnz + q] = src_idx[static_cast<uint64_t>(k) * nnz + e];
+    val[q] = src_val[e];
+  }
+}
+
+__global__ void cast_d2f_kernel(const double* __restrict__ src, float* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<float>(src[i]);
+}
+
+__global__ void cast_f2d_kernel(const float* __restrict__ src, double* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<double>(src[i]);
+}
+
+__global__ void iota32_kernel(uint32_t* p, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<uint32_t>(i);
+}
+
+unsigned grid_for(uint64_t n, int num_sms) {
+  uint64_t g = (n + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+// std::mt19937_64 seeding (the default engine state before set_rng).
+void mt_seed(uint64_t* x, uint64_t seed) {
+  x[0] = seed;
+  for (uint32_t i = 1; i < 312; ++i) x[i] = 6364136223846793005ULL * (x[i - 1] ^ (x[i - 1] >> 62)) + i;
+}
+
+template <class T>
+int dalloc(T** p, uint64_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  SGDT_CUDA(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  return SGDT_OK;
+}
+
+#define TRY(x)            \
+  do {                    \
+    int rc_ = (x);        \
+    if (rc_) return rc_;  \
+  } while (0)
+
+int validate_desc(const sgdt_tensor_desc* d, const char* what) {
+  if (!d) return fail(SGDT_ERR_DOMAIN, std::string(what) + ": null tensor");
+  if (d->order < 2 || d->order > kMaxOrder)
+    return fail(SGDT_ERR_DOMAIN, std::string(what) + ": order must be in [2, 8]");
+  if (d->nnz == 0) return fail(SGDT_ERR_DATA, std::string(what) + ": tensor has no entries");
+  if (d->nnz > 0xFFFFFFFFull)
+    return fail(SGDT_ERR_DATA, std::string(what) + ": entry count exceeds the 32-bit id space");
+  for (int k = 0; k < d->order; ++k)
+    if (d->dims[k] < 1) return fail(SGDT_ERR_DOMAIN, std::string(what) + ": every dim must be >= 1");
+  const int order = d->order;
+  for (uint64_t e = 0; e < d->nnz; ++e)
+    for (int k = 0; k < order; ++k) {
+      const uint32_t c = d->coords[e * order + k];
+      if (c < 1 || c > d->dims[k])
+        return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(e) +
+                                       ": coordinate out of range");
+    }
+  return SGDT_OK;
+}
+
+// Row offsets of mode n (CooTensor::mode_offsets, sptensor.cpp:107-111) and,
+// when no permutation is supplied, the stable counting sort itself.
+void host_mode_layout(const sgdt_tensor_desc* d, int n, std::vector<uint64_t>& off,
+                      std::vector<uint32_t>& perm) {
+  const uint32_t dim = d->dims[n];
+  const int order = d->order;
+  off.assign(static_cast<size_t>(dim) + 1, 0);
+  for (uint64_t e = 0; e < d->nnz; ++e) off[d->coords[e * order + n]]++;
+  for (size_t i = 1; i <= dim; ++i) off[i] += off[i - 1];
+  if (d->mode_perm && d->mode_perm[n]) return;
+  perm.resize(d->nnz);
+  std::vector<uint64_t> cursor(off.begin(), off.end() - 1);
+  for (uint64_t e = 0; e < d->nnz; ++e) perm[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
+}
+
+// nnz-balanced chunk schedule over the mode-sorted entries: whole rows packed
+// greedily up to chunk_size, longer rows cut into pieces of chunk_size.
+void build_chunks(const std::vector<uint64_t>& off, uint32_t chunk_size, std::vector<Chunk>& chunks,
+                  std::vector<SplitRow>& splits, uint32_t& n_pieces, uint64_t& nonempty) {
+  chunks.clear();
+  splits.clear();
+  n_pieces = 0;
+  nonempty = 0;
+  const size_t rows = off.size() - 1;
+  bool open = false;
+  Chunk cur{0, 0, -1, 0};
+  for (size_t i = 0; i < rows; ++i) {
+    const uint64_t b = off[i], e = off[i + 1], cnt = e - b;
+    if (cnt == 0) continue;
+    ++nonempty;
+    if (cnt > chunk_size) {
+      if (open) {
+        chunks.push_back(cur);
+        open = false;
+      }
+      SplitRow sr{static_cast<uint32_t>(i), n_pieces, 0, 0};
+      for (uint64_t p = b; p < e; p += chunk_size) {
+        const uint64_t pe = std::min<uint64_t>(p + chunk_size, e);
+        chunks.push_back(Chunk{static_cast<uint32_t>(p), static_cast<uint32_t>(pe),
+                               static_cast<int32_t>(n_pieces++), 0});
+        ++sr.count;
+      }
+      splits.push_back(sr);
+      continue;
+    }
+    if (open && (e - cur.begin) > chunk_size) {
+      chunks.push_back(cur);
+      open = false;
+    }
+    if (!open) {
+      cur = Chunk{static_cast<uint32_t>(b), static_cast<uint32_t>(e), -1, 0};
+      open = true;
+    } else {
+      cur.end = static_cast<uint32_t>(e);
+    }
+  }
+  if (open) chunks.push_back(cur);
+}
+
+int upload_record_copy(Session& s, const sgdt_tensor_desc* d, RecordCopy& rc, uint32_t** d_coords_keep,
+                       double** d_values_keep) {
+  const uint64_t nnz = d->nnz;
+  const int order = d->order;
+  uint32_t* d_coords;
+  double* d_values;
+  TRY(dalloc(&d_coords, nnz * order));
+  TRY(dalloc(&d_values, nnz));
+  SGDT_CUDA(cudaMemcpyAsync(d_coords, d->coords, nnz * order * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            s.stream));
+  SGDT_CUDA(cudaMemcpyAsync(d_values, d->values, nnz * sizeof(double), cudaMemcpyHostToDevice, s.stream));
+  rc.nnz = nnz;
+  TRY(dalloc(&rc.idx, nnz * order));
+  TRY(dalloc(&rc.val, nnz));
+  build_entry_copy_kernel<<<grid_for(nnz, s.num_sms), 256, 0, s.stream>>>(d_coords, d_values, nnz, order,
+                                                                           rc.idx, rc.val);
+  SGDT_CUDA(cudaGetLastError());
+  if (d_coords_keep) {
+    *d_coords_keep = d_coords;
+  } else {
+    SGDT_CUDA(cudaStreamSynchronize(s.stream));
+    cudaFree(d_coords);
+  }
+  if (d_values_keep) {
+    *d_values_keep = d_values;
+  } else {
+    SGDT_CUDA(cudaStreamSynchronize(s.stream));
+    cudaFree(d_values);
+  }
+  return SGDT_OK;
+}
+
+void free_session(sgdt_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(s->train_rec.idx);
+  F(s->train_rec.val);
+  F(s->test_rec.idx);
+  F(s->test_rec.val);
+  for (int n = 0; n < kMaxOrder; ++n) {
+    F(s->mode[n].rec.idx);
+    F(s->mode[n].rec.val);
+    F(s->mode[n].row_ptr);
+    F(s->mode[n].chunks);
+    F(s->mode[n].splits);
+    F(s->P.A[n]);
+    F(s->P.B[n]);
+    F(s->P.Q[n]);
+  }
+  F(s->piece_partials);
+  F(s->mt);
+  F(s->pool);
+  F(s->head);
+  F(s->draw_j);
+  F(s->link);
+  F(s->kprev);
+  F(s->lprev);
+  F(s->dval);
+  F(s->batch);
+  F(s->cs_a);
+  F(s->cs_c);
+  F(s->cs_xhat);
+  F(s->cs_x);
+  F(s->cs_part);
+  F(s->ev_part);
+  F(s->ev_out);
+  F(s->flag);
+  F(s->stage);
+  if (s->h_ev_out) cudaFreeHost(s->h_ev_out);
+  if (s->h_flag) cudaFreeHost(s->h_flag);
+  for (auto& e : s->ev)
+    if (e) cudaEventDestroy(e);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int ensure_batch_capacity(Session& s, uint64_t m) {
+  const uint64_t need = m * s.order;
+  if (need <= s.batch_cap) return SGDT_OK;
+  SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(s.batch);
+  F(s.draw_j);
+  F(s.link);
+  F(s.kprev);
+  F(s.lprev);
+  F(s.dval);
+  TRY(dalloc(&s.batch, need));
+  TRY(dalloc(&s.draw_j, m));
+  TRY(dalloc(&s.link, m));
+  TRY(dalloc(&s.kprev, m));
+  TRY(dalloc(&s.lprev, m));
+  TRY(dalloc(&s.dval, m));
+  s.batch_cap = need;
+  s.last_batch = nullptr;
+  s.last_batch_len = 0;
+  return SGDT_OK;
+}
+
+int ensure_core_capacity(Session& s, uint64_t m) {
+  if (m <= s.cs_cap) return SGDT_OK;
+  SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(s.cs_a);
+  F(s.cs_c);
+  F(s.cs_xhat);
+  F(s.cs_x);
+  F(s.cs_part);
+  uint32_t js = 0;
+  for (int k = 0; k < s.order; ++k) js = std::max(js, s.J[k]);
+  TRY(dalloc(&s.cs_a, m * js));
+  TRY(dalloc(&s.cs_c, m * s.RP));
+  TRY(dalloc(&s.cs_xhat, m));
+  TRY(dalloc(&s.cs_x, m));
+  TRY(dalloc(&s.cs_part, 2ull * s.num_sms * js));
+  s.cs_cap = m;
+  return SGDT_OK;
+}
+
+int check_core_hyper(const Session& s, const sgdt_core_hyper* h, uint64_t* m_out) {
+  if (!h) return fail(SGDT_ERR_DOMAIN, "core hyper is null");
+  if (h->lr < 0.0) return fail(SGDT_ERR_DOMAIN, "core learning rate must be non-negative");
+  if (!(h->reg >= 0.0) && h->lr > 0.0) return fail(SGDT_ERR_DOMAIN, "sgd_step: regularization must be non-negative");
+  const uint64_t m = h->batch_m == 0 ? s.nnz : h->batch_m;
+  if (m > s.nnz) return fail(SGDT_ERR_DOMAIN, "core batch size exceeds training nnz");
+  *m_out = m;
+  return SGDT_OK;
+}
+
+int check_factor_hyper(const sgdt_factor_hyper* h) {
+  if (!h) return fail(SGDT_ERR_DOMAIN, "factor hyper is null");
+  if (!(h->row_fraction > 0.0 && h->row_fraction <= 1.0))
+    return fail(SGDT_ERR_DOMAIN, "row fraction must lie in (0,1]");
+  if (h->lr < 0.0) return fail(SGDT_ERR_DOMAIN, "factor learning rate must be non-negative");
+  if (h->lr > 0.0 && h->reg < 0.0) return fail(SGDT_ERR_DOMAIN, "sgd_step: regularization must be non-negative");
+  if (h->lr > 0.0 && h->row_fraction < 1.0)
+    return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not implemented on the device path yet");
+  return SGDT_OK;
+}
+
+// Enqueue one core phase (no host sync).
+int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m) {
+  if (h.lr == 0.0) return SGDT_OK;  // frozen phase: bit-exact no-op, no RNG
+  TRY(ensure_batch_capacity(s, m));
+  TRY(ensure_core_capacity(s, m));
+  const bool per_mode = h.resample_per_mode && h.batch_m != 0;
+  if (h.batch_m == 0) {
+    iota32_kernel<<<grid_for(m, s.num_sms), 256, 0, s.stream>>>(s.batch, m);
+    SGDT_CUDA(cudaGetLastError());
+    s.last_batch = s.batch;
+    s.last_batch_len = m;
+  } else {
+    const int draws = per_mode ? s.order : 1;
+    for (int n = 0; n < draws; ++n) TRY(launch_sampler(s, m, s.batch + static_cast<uint64_t>(n) * m));
+  }
+  return launch_core(s, h, s.batch, m, per_mode ? 1 : 0);
+}
+
+int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
+  if (h.lr == 0.0) return SGDT_OK;
+  for (int n = 0; n < s.order; ++n) {
+    if (time_modes) SGDT_CUDA(cudaEventRecord(s.ev[4 + n], s.stream));
+    TRY(launch_factor_mode(s, n, h));
+  }
+  return SGDT_OK;
+}
+
+int sync_and_flag(Session& s) {
+  SGDT_CUDA(cudaMemcpyAsync(s.h_flag, s.flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  if (*s.h_flag) {
+    SGDT_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), s.stream));
+    return fail(SGDT_ERR_NUMERIC, "sgd_step: non-finite parameter or gradient; reduce the learning rate");
+  }
+  return SGDT_OK;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+}  // namespace sgdt
+
+using namespace sgdt;
+
+extern "C" {
+
+const char* sgdt_last_error(void) { return g_error.c_str(); }
+const char* sgdt_version(void) { return "sgdt 0.1 (sm_100a)"; }
+
+void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uint64_t* ends) {
+  const uint64_t base = count / workers, rem = count % workers;
+  uint64_t at = 0;
+  for (uint64_t w = 0; w < workers; ++w) {
+    const uint64_t len = base + (w < rem ? 1 : 0);
+    begins[w] = at;
+    ends[w] = at + len;
+    at += len;
+  }
+}
+
+int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test, const uint32_t* J,
+                        uint32_t R, int device, sgdt_session** out) {
+  if (!out) return fail(SGDT_ERR_DOMAIN, "out is null");
+  *out = nullptr;
+  TRY(validate_desc(train, "train"));
+  if (test) {
+    TRY(validate_desc(test, "test"));
+    if (test->order != train->order) return fail(SGDT_ERR_DOMAIN, "rmse_mae: order mismatch between model and data");
+    for (int k = 0; k < train->order; ++k)
+      if (test->dims[k] > train->dims[k])
+        return fail(SGDT_ERR_DOMAIN, "rmse_mae: data exceeds the model's shape in mode " + std::to_string(k + 1));
+  }
+  if (!J) return fail(SGDT_ERR_DOMAIN, "ranks: J is null");
+  if (R < 1) return fail(SGDT_ERR_DOMAIN, "ranks: R_core must be >= 1");
+  if (R > SGDT_MAX_RCORE) return fail(SGDT_ERR_CONFIG, "R_core > 32 is not supported by the device kernels");
+  for (int k = 0; k < train->order; ++k) {
+    if (J[k] < 1) return fail(SGDT_ERR_DOMAIN, "ranks: every J_n must be >= 1");
+    if (J[k] < R) return fail(SGDT_ERR_DOMAIN, "ranks: R_core must satisfy R_core <= J_n");
+    if (J[k] > SGDT_MAX_J) return fail(SGDT_ERR_CONFIG, "J_n > 64 is not supported by the device kernels");
+  }
+  if (device >= 0) SGDT_CUDA(cudaSetDevice(device));
+  auto* s = new sgdt_session();
+  SGDT_CUDA(cudaGetDevice(&s->device));
+  cudaDeviceProp prop{};
+  SGDT_CUDA(cudaGetDeviceProperties(&prop, s->device));
+  s->num_sms = prop.multiProcessorCount;
+  int rc = [&]() -> int {
+    SGDT_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    for (auto& e : s->ev) SGDT_CUDA(cudaEventCreate(&e));
+    if (const char* cs = std::getenv("SGDT_CHUNK_SIZE")) {
+      const long v = std::strtol(cs, nullptr, 10);
+      if (v >= 1 && v <= (1L << 24)) s->chunk_size = static_cast<uint32_t>(v);
+    }
+    s->order = train->order;
+    s->nnz = train->nnz;
+    s->R = R;
+    s->RP = (R + 3) & ~3u;
+    s->P.order = s->order;
+    s->P.R = R;
+    s->P.RP = s->RP;
+    for (int k = 0; k < s->order; ++k) {
+      s->dims[k] = s->P.dims[k] = train->dims[k];
+      s->J[k] = s->P.J[k] = J[k];
+    }
+    // records: entry order (kept for Psi gathers + train RMSE) and per mode
+    TRY(upload_record_copy(*s, train, s->train_rec, nullptr, nullptr));
+    uint32_t max_pieces = 0;
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> perm;
+    uint32_t* d_perm = nullptr;
+    TRY(dalloc(&d_perm, s->nnz));
+    for (int n = 0; n < s->order; ++n) {
+      ModePlan& mp = s->mode[n];
+      host_mode_layout(train, n, off, perm);
+      const uint32_t* hperm = (train->mode_perm && train->mode_perm[n]) ? train->mode_perm[n] : perm.data();
+      SGDT_CUDA(cudaMemcpyAsync(d_perm, hperm, s->nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+      mp.rec.nnz = s->nnz;
+      TRY(dalloc(&mp.rec.idx, s->nnz * s->order));
+      TRY(dalloc(&mp.rec.val, s->nnz));
+      gather_mode_copy_kernel<<<grid_for(s->nnz, s->num_sms), 256, 0, s->stream>>>(
+          s->train_rec.idx, s->train_rec.val, d_perm, s->nnz, s->order, mp.rec.idx, mp.rec.val);
+      SGDT_CUDA(cudaGetLastError());
+      std::vector<uint32_t> rp(off.size());
+      for (size_t i = 0; i < off.size(); ++i) rp[i] = static_cast<uint32_t>(off[i]);
+      TRY(dalloc(&mp.row_ptr, rp.size()));
+      SGDT_CUDA(cudaMemcpyAsync(mp.row_ptr, rp.data(), rp.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                s->stream));
+      std::vector<Chunk> chunks;
+      std::vector<SplitRow> splits;
+      build_chunks(off, s->chunk_size, chunks, splits, mp.n_pieces, mp.rows_nonempty);
+      mp.rows_empty = s->dims[n] - mp.rows_nonempty;
+      mp.n_chunks = static_cast<uint32_t>(chunks.size());
+      mp.n_splits = static_cast<uint32_t>(splits.size());
+      TRY(dalloc(&mp.chunks, chunks.size()));
+      TRY(dalloc(&mp.splits, splits.size()));
+      if (!chunks.empty())
+        SGDT_CUDA(cudaMemcpyAsync(mp.chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice,
+                                  s->stream));
+      if (!splits.empty())
+        SGDT_CUDA(cudaMemcpyAsync(mp.splits, splits.data(), splits.size() * sizeof(SplitRow),
+                                  cudaMemcpyHostToDevice, s->stream));
+      max_pieces = std::max(max_pieces, mp.n_pieces);
+      SGDT_CUDA(cudaStreamSynchronize(s->stream));  // host vectors are reused
+    }
+    cudaFree(d_perm);
+    if (test) {
+      s->nnz_test = test->nnz;
+      TRY(upload_record_copy(*s, test, s->test_rec, nullptr, nullptr));
+    }
+    // model
+    uint64_t stage = 0;
+    for (int k = 0; k < s->order; ++k) {
+      TRY(dalloc(&s->P.A[k], static_cast<uint64_t>(s->dims[k]) * s->J[k]));
+      TRY(dalloc(&s->P.B[k], static_cast<uint64_t>(s->J[k]) * R));
+      TRY(dalloc(&s->P.Q[k], static_cast<uint64_t>(s->dims[k]) * s->RP));
+      SGDT_CUDA(cudaMemsetAsync(s->P.A[k], 0, static_cast<uint64_t>(s->dims[k]) * s->J[k] * sizeof(float), s->stream));
+      SGDT_CUDA(cudaMemsetAsync(s->P.B[k], 0, static_cast<uint64_t>(s->J[k]) * R * sizeof(float), s->stream));
+      SGDT_CUDA(cudaMemsetAsync(s->P.Q[k], 0, static_cast<uint64_t>(s->dims[k]) * s->RP * sizeof(float), s->stream));
+      stage = std::max<uint64_t>(stage, static_cast<uint64_t>(s->dims[k]) * s->J[k]);
+    }
+    TRY(dalloc(&s->stage, stage));
+    s->stage_cap = stage;
+    TRY(dalloc(&s->piece_partials, static_cast<uint64_t>(std::max<uint32_t>(max_pieces, 1)) * s->RP));
+    // sampler
+    TRY(dalloc(&s->mt, 313));
+    uint64_t mt[313];
+    mt_seed(mt, 5489u);
+    mt[312] = 312;
+    SGDT_CUDA(cudaMemcpy(s->mt, mt, sizeof mt, cudaMemcpyHostToDevice));
+    TRY(dalloc(&s->pool, s->nnz));
+    TRY(dalloc(&s->head, s->nnz));
+    SGDT_CUDA(cudaMemsetAsync(s->head, 0, s->nnz * sizeof(unsigned long long), s->stream));
+    // eval + flag
+    TRY(dalloc(&s->ev_part, 2ull * s->num_sms * 8));
+    TRY(dalloc(&s->ev_out, 2));
+    TRY(dalloc(&s->flag, 1));
+    SGDT_CUDA(cudaMemsetAsync(s->flag, 0, sizeof(int), s->stream));
+    SGDT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_ev_out), 2 * sizeof(double), cudaHostAllocDefault));
+    SGDT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_flag), sizeof(int), cudaHostAllocDefault));
+    SGDT_CUDA(cudaStreamSynchronize(s->stream));
+    return SGDT_OK;
+  }();
+  if (rc) {
+    const std::string keep = g_error;
+    free_session(s);
+    g_error = keep;
+    return rc;
+  }
+  *out = s;
+  return SGDT_OK;
+}
+
+void sgdt_session_destroy(sgdt_session* s) { free_session(s); }
+
+void* sgdt_session_stream(sgdt_session* s) { return s ? static_cast<void*>(s->stream) : nullptr; }
+
+int sgdt_set_model(sgdt_session* s, const double* const* A, const double* const* B) {
+  if (!s || !A || !B) return fail(SGDT_ERR_DOMAIN, "set_model: null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  for (int k = 0; k < s->order; ++k) {
+    const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k];
+    const uint64_t nb = static_cast<uint64_t>(s->J[k]) * s->R;
+    SGDT_CUDA(cudaMemcpyAsync(s->stage, A[k], na * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    cast_d2f_kernel<<<grid_for(na, s->num_sms), 256, 0, s->stream>>>(s->stage, s->P.A[k], na);
+    SGDT_CUDA(cudaMemcpyAsync(s->stage, B[k], nb * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    cast_d2f_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->stage, s->P.B[k], nb);
+    SGDT_CUDA(cudaGetLastError());
+  }
+  for (int k = 0; k < s->order; ++k) TRY(launch_q_refresh(*s, k));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_get_model(sgdt_session* s, double* const* A, double* const* B) {
+  if (!s || !A || !B) return fail(SGDT_ERR_DOMAIN, "get_model: null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  for (int k = 0; k < s->order; ++k) {
+    const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k];
+    const uint64_t nb = static_cast<uint64_t>(s->J[k]) * s->R;
+    cast_f2d_kernel<<<grid_for(na, s->num_sms), 256, 0, s->stream>>>(s->P.A[k], s->stage, na);
+    SGDT_CUDA(cudaMemcpyAsync(A[k], s->stage, na * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    cast_f2d_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->P.B[k], s->stage, nb);
+    SGDT_CUDA(cudaMemcpyAsync(B[k], s->stage, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    SGDT_CUDA(cudaGetLastError());
+  }
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_set_rng(sgdt_session* s, const uint64_t* mt312, uint32_t pos) {
+  if (!s || !mt312) return fail(SGDT_ERR_DOMAIN, "set_rng: null argument");
+  if (pos > 312) return fail(SGDT_ERR_DOMAIN, "set_rng: position out of range");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  uint64_t st[313];
+  std::memcpy(st, mt312, 312 * sizeof(uint64_t));
+  st[312] = pos;
+  SGDT_CUDA(cudaMemcpyAsync(s->mt, st, sizeof st, cudaMemcpyHostToDevice, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_get_rng(sgdt_session* s, uint64_t* mt312, uint32_t* pos) {
+  if (!s || !mt312 || !pos) return fail(SGDT_ERR_DOMAIN, "get_rng: null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  uint64_t st[313];
+  SGDT_CUDA(cudaMemcpyAsync(st, s->mt, sizeof st, cudaMemcpyDeviceToHost, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  std::memcpy(mt312, st, 312 * sizeof(uint64_t));
+  *pos = static_cast<uint32_t>(st[312]);
+  return SGDT_OK;
+}
+
+int sgdt_reset_pool(sgdt_session* s) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  s->pool_valid = false;
+  return SGDT_OK;
+}
+
+int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (m < 1 || m > s->nnz) return fail(SGDT_ERR_DOMAIN, "sample_batch: batch size out of range");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(ensure_batch_capacity(*s, m));
+  TRY(launch_sampler(*s, m, s->batch));
+  if (out) SGDT_CUDA(cudaMemcpyAsync(out, s->batch, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_last_batch(sgdt_session* s, uint32_t* out, uint64_t* len) {
+  if (!s || !len) return fail(SGDT_ERR_DOMAIN, "null argument");
+  *len = s->last_batch_len;
+  if (out && s->last_batch_len) {
+    SGDT_CUDA(cudaMemcpyAsync(out, s->last_batch, s->last_batch_len * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                              s->stream));
+    SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  return SGDT_OK;
+}
+
+int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* st) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, h, &m));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (st) {
+    st->batch_size = h->lr == 0.0 ? 0 : m;
+    st->effective_workers = h->lr == 0.0 ? 0 : 1;
+  }
+  if (h->lr == 0.0) return SGDT_OK;
+  TRY(enqueue_core(*s, *h, m));
+  return sync_and_flag(*s);
+}
+
+int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_stats* st) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  TRY(check_factor_hyper(h));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (st) {
+    *st = sgdt_factor_stats{0, 0, 0.0};
+    if (h->lr > 0.0)
+      for (int n = 0; n < s->order; ++n) {
+        st->rows_updated += s->mode[n].rows_nonempty;
+        st->rows_skipped += s->mode[n].rows_empty;
+      }
+  }
+  if (h->lr == 0.0) return SGDT_OK;
+  TRY(enqueue_factor(*s, *h, false));
+  return sync_and_flag(*s);
+}
+
+int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, ch, &m));
+  TRY(check_factor_hyper(fh));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  const bool timed = true;
+  for (uint64_t e = 0; e < epochs; ++e) {
+    const bool last = e + 1 == epochs;
+    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[0], s->stream));
+    TRY(enqueue_core(*s, *ch, m));
+    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[1], s->stream));
+    TRY(enqueue_factor(*s, *fh, last && timed));
+    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
+  }
+  TRY(sync_and_flag(*s));
+  if (epochs > 0) {
+    sgdt_timing t{};
+    SGDT_CUDA(cudaEventElapsedTime(&t.core_ms, s->ev[0], s->ev[1]));
+    SGDT_CUDA(cudaEventElapsedTime(&t.factor_ms, s->ev[1], s->ev[2]));
+    if (fh->lr > 0.0)
+      for (int n = 0; n < s->order; ++n)
+        SGDT_CUDA(cudaEventElapsedTime(&t.factor_mode_ms[n], s->ev[4 + n],
+                                       n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2]));
+    s->timing = t;
+    s->timing_valid = true;
+  }
+  return SGDT_OK;
+}
+
+int sgdt_eval(sgdt_session* s, int which, double* rmse, double* mae) {
+  if (!s || !rmse || !mae) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (which != 0 && which != 1) return fail(SGDT_ERR_DOMAIN, "eval: which must be 0 (train) or 1 (test)");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  return launch_eval(*s, which, rmse, mae);
+}
+
+int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
+               double* metrics) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  for (uint64_t e = 0; e < epochs; ++e) {
+    TRY(sgdt_run_epochs(s, ch, fh, 1));
+    double* row = metrics ? metrics + e * 6 : nullptr;
+    if (row) {
+      row[0] = s->timing.core_ms * 1e-3;
+      row[1] = s->timing.factor_ms * 1e-3;
+      TRY(sgdt_eval(s, 0, &row[2], &row[3]));
+      if (s->nnz_test) {
+        TRY(sgdt_eval(s, 1, &row[4], &row[5]));
+      } else {
+        row[4] = row[5] = std::nan("");
+      }
+    }
+  }
+  return SGDT_OK;
+}
+
+int sgdt_last_timing(sgdt_session* s, sgdt_timing* t) {
+  if (!s || !t) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (!s->timing_valid) return fail(SGDT_ERR_DOMAIN, "no epoch has been timed yet");
+  *t = s->timing;
+  return SGDT_OK;
+}
+
+}  // extern "C"

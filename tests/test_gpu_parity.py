@@ -1,0 +1,292 @@
+"""GPU parity of the B200 path (libsgdt.so through the C-ABI) vs the oracle.
+
+Bars (BASELINE.json north_star):
+  * sampling / permutation: bit-exact with the reference sampler;
+  * per-epoch factor and core values: rel_err <= 1e-4, with
+    rel_err = |g - ref| / max(1, |ref|)  (oracle.cpp:409-411), teacher-forced
+    from the same fp32-representable state;
+  * final test RMSE within 1e-3 of the oracle's.
+The oracle (oracle/sgdt_oracle.c) is pinned bit-for-bit against the reference
+by tests/test_oracle_pin.py.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle_py as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def sg():
+    from paper_2012_03550_b200 import sgdt
+    return sgdt
+
+
+def rel_err(g, ref):
+    g = np.asarray(g, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(g - ref) / np.maximum(1.0, np.abs(ref)))) if g.size else 0.0
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+def make_case(dims, J, R, nnz, seed, noise=0.05, tm=0.5, ts=0.1, split=None):
+    c, v = O.synth_planted(dims, J, R, nnz, noise, tm, ts, seed)
+    if split:
+        trc, trv, tec, tev = O.train_test_split(dims, c, v, split, 1)
+        return (trc, trv), (tec, tev)
+    return (c, v), None
+
+
+def session_for(dims, tr, J, R, te=None):
+    return sg().Session(dims, tr[0], tr[1], J, R, test=te)
+
+
+def oracle_model(dims, J, R, seed, sd=0.2):
+    m = O.Model(dims, J, R).init_gaussian(0.5, sd, seed)
+    A, B = m.params()
+    m.set_params([f32(a) for a in A], [f32(b) for b in B])  # fp32-representable start
+    return m
+
+
+# ---------------------------------------------------------------- sampler
+@pytest.mark.parametrize("m", [1, 7, 100, 1024])
+def test_sampler_bit_exact_with_persistent_pool(m):
+    dims = (60, 50, 40)
+    tr, _ = make_case(dims, (3, 3, 3), 3, 3000, 1)
+    s = session_for(dims, tr, (3, 3, 3), 3)
+    s.seed(42)
+    r = O.Rng(42)
+    ws = O.CoreWorkspace(3000)
+    for _ in range(25):
+        got = s.sample_batch(m)
+        ref = O.sample_batch(3000, m, r, ws)
+        assert np.array_equal(got, ref)
+    st, pos = s.get_rng()
+    rst, rpos = r.state()
+    assert pos == rpos and np.array_equal(st, rst)
+
+
+def test_sampler_full_permutation_and_small_sets():
+    dims = (10, 1)
+    coords = np.array([[i + 1, 1] for i in range(10)], np.uint32)
+    s = sg().Session(dims, coords, np.ones(10), (1, 1), 1)
+    s.seed(5)
+    r = O.Rng(5)
+    ws = O.CoreWorkspace(10)
+    for m in (10, 1, 10, 3, 10):
+        got = s.sample_batch(m)
+        assert np.array_equal(got, O.sample_batch(10, m, r, ws))
+    assert sorted(s.sample_batch(10).tolist()) == list(range(10))
+    with pytest.raises(sg().DomainError):
+        s.sample_batch(11)
+    with pytest.raises(sg().DomainError):
+        s.sample_batch(0)
+
+
+def test_sampler_large_batch_collisions():
+    # m close to nnz forces long swap chains through the parallel resolution
+    dims = (40, 40, 40)
+    tr, _ = make_case(dims, (2, 2, 2), 2, 5000, 3)
+    s = session_for(dims, tr, (2, 2, 2), 2)
+    s.seed(7)
+    r = O.Rng(7)
+    ws = O.CoreWorkspace(5000)
+    for m in (4999, 2500, 5000, 4000):
+        assert np.array_equal(s.sample_batch(m), O.sample_batch(5000, m, r, ws))
+
+
+def test_next_below_rejection_path_bit_exact():
+    # bounds near 2^63 reject about half of all raw outputs
+    rs = np.random.default_rng(0)
+    bounds = np.concatenate([np.full(400, 2**63 + 12345, np.uint64),
+                             rs.integers(1, 2**40, 300, dtype=np.uint64),
+                             np.full(300, 2**64 - 3, np.uint64)])
+    rs.shuffle(bounds)
+    st, pos = sg().mt19937_64_state(99)
+    got, st2, pos2 = sg().rng_next_below(st, pos, bounds)
+    r = O.Rng(99)
+    ref = np.array([r.next_below(int(b)) for b in bounds], np.uint64)
+    assert np.array_equal(got, ref)
+    rst, rpos = r.state()
+    assert pos2 == rpos and np.array_equal(st2, rst)
+
+
+# ---------------------------------------------------------------- eval
+def test_rmse_mae_matches_oracle():
+    dims = (30, 25, 20)
+    tr, te = make_case(dims, (3, 3, 3), 3, 4000, 5, noise=0.5, split=0.1)
+    m = oracle_model(dims, (3, 3, 3), 3, 11)
+    s = session_for(dims, tr, (3, 3, 3), 3, te=te)
+    s.set_model(*m.params())
+    for which, t in ((0, tr), (1, te)):
+        got = s.eval(which)
+        ref = O.rmse_mae(m, O.Tensor(dims, *t))
+        assert abs(got[0] - ref[0]) <= 1e-5 * max(1.0, ref[0])
+        assert abs(got[1] - ref[1]) <= 1e-5 * max(1.0, ref[1])
+
+
+def test_rmse_fixed_errors():
+    # predictions all zero, values {0, 2} -> RMSE sqrt(2), MAE 1 (test_eval.cpp:32-41)
+    coords = np.array([[1, 1], [2, 1]], np.uint32)
+    s = sg().Session((2, 1), coords, np.array([0.0, 2.0]), (2, 2), 2)
+    s.set_model([np.zeros((2, 2)), np.zeros((1, 2))], [np.zeros((2, 2)), np.zeros((2, 2))])
+    rm, ma = s.eval(0)
+    assert abs(rm - np.sqrt(2.0)) < 1e-12 and abs(ma - 1.0) < 1e-12
+
+
+# ---------------------------------------------------------------- epochs
+CASES = [
+    dict(dims=(12, 10, 8), J=(3, 3, 3), R=2, nnz=300, batch_m=16),
+    dict(dims=(40, 30, 20), J=(5, 5, 5), R=5, nnz=5000, batch_m=256),
+    dict(dims=(12, 10, 8), J=(3, 4, 3), R=3, nnz=300, batch_m=0),
+    dict(dims=(9, 7, 6, 5), J=(2, 3, 2, 2), R=2, nnz=400, batch_m=50, resample=True),
+    dict(dims=(30, 25), J=(3, 3), R=3, nnz=220, batch_m=20, incremental=True),
+    dict(dims=(8, 7, 6, 5, 4), J=(3, 3, 3, 3, 3), R=3, nnz=1500, batch_m=100),
+    dict(dims=(6, 300, 300), J=(8, 8, 8), R=8, nnz=30000, batch_m=2048),  # split rows
+    dict(dims=(50, 40, 30), J=(10, 10, 10), R=10, nnz=8000, batch_m=1024),
+    dict(dims=(20, 20, 20), J=(16, 12, 16), R=12, nnz=3000, batch_m=300),
+    dict(dims=(20, 20, 20), J=(32, 32, 32), R=32, nnz=3000, batch_m=300),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c["dims"])) + f"_R{c['R']}")
+def test_epoch_teacher_forced_parity(case):
+    dims, J, R, nnz = case["dims"], case["J"], case["R"], case["nnz"]
+    bm = case["batch_m"]
+    tr, _ = make_case(dims, J, min(J), nnz, 17)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 23)
+    rng = O.Rng(5)
+    ws = O.CoreWorkspace(nnz)
+    s.set_rng(*rng.state())
+    lr, reg = 0.01, 0.01
+    for epoch in range(2):
+        s.set_model(*m.params())  # teacher forcing: same fp32 start each step
+        s.core_epoch(lr, reg, bm, case.get("resample", False), case.get("incremental", False))
+        O.update_core_epoch(m, t, lr, reg, bm, rng, ws, case.get("resample", False),
+                            case.get("incremental", False))
+        if bm:
+            assert np.array_equal(s.last_batch(), ws.batch())
+        A, B = s.get_model()
+        RA, RB = m.params()
+        for n in range(len(dims)):
+            assert rel_err(B[n], RB[n]) <= TOL, f"core B^({n}) epoch {epoch}"
+        m.set_params([f32(a) for a in RA], [f32(b) for b in RB])
+        s.set_model(*m.params())
+        up, sk = s.factor_epoch(lr, reg)
+        rup, rsk = O.update_factor_epoch(m, t, lr, reg, rng)
+        assert (up, sk) == (rup, rsk)
+        A, B = s.get_model()
+        RA, RB = m.params()
+        for n in range(len(dims)):
+            assert rel_err(A[n], RA[n]) <= TOL, f"factor A^({n}) epoch {epoch}"
+            assert np.array_equal(B[n], RB[n])
+        m.set_params([f32(a) for a in RA], [f32(b) for b in RB])
+        st, pos = s.get_rng()
+        rst, rpos = rng.state()
+        assert pos == rpos and np.array_equal(st, rst)
+
+
+def test_small_chunks_force_row_splitting(monkeypatch):
+    monkeypatch.setenv("SGDT_CHUNK_SIZE", "40")
+    dims = (5, 60, 50)
+    J, R = (4, 4, 4), 4
+    tr, _ = make_case(dims, J, R, 6000, 29)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 31)
+    s.set_model(*m.params())
+    s.factor_epoch(0.01, 0.01)
+    O.update_factor_epoch(m, t, 0.01, 0.01, O.Rng(1))
+    A, _ = s.get_model()
+    RA, _ = m.params()
+    for n in range(3):
+        assert rel_err(A[n], RA[n]) <= TOL
+
+
+def test_free_run_config1_matches_reference_rmse():
+    """BASELINE config 1 end to end (10 epochs); the reference's own final
+    test RMSE is committed in tests/golden/config1.json."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config1.json")))
+    sp, h = g["spec"], g["hyper"]
+    c, v = O.synth_planted(sp["dims"], sp["tJ"], sp["tR"], sp["nnz"], sp["noise"], sp["tmean"],
+                           sp["tsd"], sp["seed"])
+    trc, trv, tec, tev = O.train_test_split(sp["dims"], c, v, 0.1, 1)
+    s = sg().Session(sp["dims"], trc, trv, h["J"], h["R"], test=(tec, tev))
+    m = O.Model(sp["dims"], h["J"], h["R"]).init_gaussian(0.5, 0.1, h["seed"])
+    s.set_model(*m.params())
+    s.seed(h["seed"] + 1)
+    met = s.train(sg().CoreHyper(h["lr_b"], h["reg_b"], h["batch_m"], 0, 0),
+                  sg().FactorHyper(h["lr_a"], h["reg_a"], 1.0), h["epochs"])
+    assert abs(met[-1, 4] - g["test_rmse"][-1]) <= 1e-3
+    assert abs(met[-1, 2] - g["train_rmse"][-1]) <= 1e-3
+    for e in range(h["epochs"]):
+        assert abs(met[e, 4] - g["test_rmse"][e]) <= 1e-3
+
+
+def test_lr_zero_freezes_bit_exact_and_consumes_no_rng():
+    dims = (12, 10, 8)
+    tr, _ = make_case(dims, (3, 3, 3), 3, 300, 2)
+    s = session_for(dims, tr, (3, 3, 3), 3)
+    m = oracle_model(dims, (3, 3, 3), 3, 4)
+    s.set_model(*m.params())
+    s.seed(3)
+    A0, B0 = s.get_model()
+    assert s.core_epoch(0.0, 0.01, 16) == (0, 0)
+    assert s.factor_epoch(0.0, 0.01) == (0, 0)
+    A1, B1 = s.get_model()
+    for n in range(3):
+        assert np.array_equal(A0[n], A1[n]) and np.array_equal(B0[n], B1[n])
+    st, pos = s.get_rng()
+    st0, pos0 = sg().mt19937_64_state(3)
+    assert pos == pos0 and np.array_equal(st, st0)
+
+
+def test_divergence_raises_numeric_error():
+    dims = (12, 10, 8)
+    tr, _ = make_case(dims, (3, 3, 3), 3, 300, 2)
+    s = session_for(dims, tr, (3, 3, 3), 3)
+    m = oracle_model(dims, (3, 3, 3), 3, 4)
+    s.set_model(*m.params())
+    with pytest.raises(sg().NumericError):
+        for _ in range(50):
+            s.factor_epoch(1e30, 0.01)
+
+
+def test_hyper_errors():
+    dims = (12, 10, 8)
+    tr, _ = make_case(dims, (3, 3, 3), 3, 300, 2)
+    s = session_for(dims, tr, (3, 3, 3), 3)
+    with pytest.raises(sg().DomainError):
+        s.core_epoch(0.01, 0.01, 301)  # M > nnz
+    with pytest.raises(sg().DomainError):
+        s.core_epoch(-1.0, 0.01, 10)
+    with pytest.raises(sg().DomainError):
+        s.factor_epoch(0.01, 0.01, 0.0)
+    with pytest.raises(sg().DataError):
+        sg().Session(dims, np.array([[13, 1, 1]], np.uint32), np.ones(1), (3, 3, 3), 3)
+
+
+def test_run_to_run_bit_identical():
+    dims = (6, 300, 300)
+    tr, _ = make_case(dims, (8, 8, 8), 8, 30000, 13)
+    outs = []
+    for _ in range(2):
+        s = session_for(dims, tr, (8, 8, 8), 8)
+        m = oracle_model(dims, (8, 8, 8), 8, 19)
+        s.set_model(*m.params())
+        s.seed(77)
+        s.run_epochs(sg().CoreHyper(0.01, 0.01, 2048, 0, 0), sg().FactorHyper(0.01, 0.01, 1.0), 3)
+        outs.append(s.get_model())
+    for n in range(3):
+        assert np.array_equal(outs[0][0][n], outs[1][0][n])
+        assert np.array_equal(outs[0][1][n], outs[1][1][n])
