@@ -159,11 +159,11 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
           V += __ldcg(part + static_cast<uint64_t>(b) * a.js + tid);
         const float bold = bs[n][tid * RP + rc];
         double w = static_cast<double>(bold);
-        int bad = !isfinite(w) || !isfinite(V);
+        int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
         w -= a.lr * (V * inv_m + a.reg * w);
         const float bnew = static_cast<float>(w);
-        bad |= !isfinite(bnew);
-        if (bad && blockIdx.x == 0) atomicOr(a.flag, 1);
+        bad |= !isfinite(bnew) ? 4 : 0;
+        if (bad && blockIdx.x == 0) atomicOr(a.flag, bad);
         dbv[tid] = bnew - bold;
         bs[n][tid * RP + rc] = bnew;
       }

@@ -85,7 +85,7 @@ __device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row
   float4* dst = reinterpret_cast<float4*>(a.P.Q[a.n] + static_cast<uint64_t>(row) * RP);
 #pragma unroll
   for (int r = 0; r < RP; r += 4) dst[r / 4] = make_float4(q[r], q[r + 1], q[r + 2], q[r + 3]);
-  if (bad) atomicOr(a.flag, 1);
+  if (bad) atomicOr(a.flag, 8);
 }
 
 template <int RP>

@@ -136,9 +136,11 @@ int fail(int code, const std::string& msg);
 #define SGDT_CUDA(call)                                                              \
   do {                                                                               \
     cudaError_t e_ = (call);                                                         \
-    if (e_ != cudaSuccess)                                                           \
+    if (e_ != cudaSuccess) {                                                         \
+      (void)cudaGetLastError(); /* clear a non-sticky error for the next call */     \
       return ::sgdt::fail(SGDT_ERR_INTERNAL, std::string(#call) + ": " +             \
                                                 cudaGetErrorString(e_));             \
+    }                                                                                \
   } while (0)
 
 // kernels (launchers return cudaError_t)

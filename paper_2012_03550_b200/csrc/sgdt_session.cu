@@ -354,9 +354,10 @@ int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
 int sync_and_flag(Session& s) {
   SGDT_CUDA(cudaMemcpyAsync(s.h_flag, s.flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   SGDT_CUDA(cudaStreamSynchronize(s.stream));
-  if (*s.h_flag) {
+  if (*s.h_flag && !std::getenv("SGDT_DEBUG_IGNORE_FLAG")) {
     SGDT_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), s.stream));
-    return fail(SGDT_ERR_NUMERIC, "sgd_step: non-finite parameter or gradient; reduce the learning rate");
+    return fail(SGDT_ERR_NUMERIC, "sgd_step: non-finite parameter or gradient; reduce the learning rate (flag " +
+                                      std::to_string(*s.h_flag) + ")");
   }
   return SGDT_OK;
 }
@@ -488,6 +489,7 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
       SGDT_CUDA(cudaMemsetAsync(s->P.B[k], 0, static_cast<uint64_t>(s->J[k]) * R * sizeof(float), s->stream));
       SGDT_CUDA(cudaMemsetAsync(s->P.Q[k], 0, static_cast<uint64_t>(s->dims[k]) * s->RP * sizeof(float), s->stream));
       stage = std::max<uint64_t>(stage, static_cast<uint64_t>(s->dims[k]) * s->J[k]);
+      stage = std::max<uint64_t>(stage, static_cast<uint64_t>(s->J[k]) * R);
     }
     TRY(dalloc(&s->stage, stage));
     s->stage_cap = stage;

@@ -48,8 +48,13 @@ def session_for(dims, tr, J, R, te=None):
     return sg().Session(dims, tr[0], tr[1], J, R, test=te)
 
 
-def oracle_model(dims, J, R, seed, sd=0.2):
-    m = O.Model(dims, J, R).init_gaussian(0.5, sd, seed)
+def unit_sigma(dims, J, R):
+    """Teacher / init scale that gives the planted xhat unit variance."""
+    return (min(J) * R ** (1.0 / len(dims))) ** -0.25
+
+
+def oracle_model(dims, J, R, seed, sd=0.2, mean=0.5):
+    m = O.Model(dims, J, R).init_gaussian(mean, sd, seed)
     A, B = m.params()
     m.set_params([f32(a) for a in A], [f32(b) for b in B])  # fp32-representable start
     return m
@@ -160,10 +165,11 @@ CASES = [
 def test_epoch_teacher_forced_parity(case):
     dims, J, R, nnz = case["dims"], case["J"], case["R"], case["nnz"]
     bm = case["batch_m"]
-    tr, _ = make_case(dims, J, min(J), nnz, 17)
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, min(J), nnz, 17, tm=0.0, ts=sig)
     t = O.Tensor(dims, *tr)
     s = session_for(dims, tr, J, R)
-    m = oracle_model(dims, J, R, 23)
+    m = oracle_model(dims, J, R, 23, sd=sig, mean=0.0)
     rng = O.Rng(5)
     ws = O.CoreWorkspace(nnz)
     s.set_rng(*rng.state())
@@ -278,11 +284,12 @@ def test_hyper_errors():
 
 def test_run_to_run_bit_identical():
     dims = (6, 300, 300)
-    tr, _ = make_case(dims, (8, 8, 8), 8, 30000, 13)
+    sig = unit_sigma(dims, (8, 8, 8), 8)
+    tr, _ = make_case(dims, (8, 8, 8), 8, 30000, 13, tm=0.0, ts=sig)
     outs = []
     for _ in range(2):
         s = session_for(dims, tr, (8, 8, 8), 8)
-        m = oracle_model(dims, (8, 8, 8), 8, 19)
+        m = oracle_model(dims, (8, 8, 8), 8, 19, sd=sig, mean=0.0)
         s.set_model(*m.params())
         s.seed(77)
         s.run_epochs(sg().CoreHyper(0.01, 0.01, 2048, 0, 0), sg().FactorHyper(0.01, 0.01, 1.0), 3)
