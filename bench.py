@@ -1,0 +1,369 @@
+"""Benchmark: sampled-nnz SGD updates/sec of the SGD_Tucker training epoch.
+
+Metric (BASELINE.json / BASELINE.md section 2): one unit is one (nonzero, mode)
+gradient visit; units per epoch = N * (M + nnz_train); throughput =
+units / (core_s + factor_s), RMSE evaluation excluded (trainer.cpp:94-107).
+A "step" is one training epoch (core phase + factor phase) over the resident
+training tensor.
+
+Workload: BASELINE config 2 (configs[1]) -- 480,000 x 17,800 x 2,200, 100M
+nonzeros, Zipf(1.1) on modes 1-2, uniform mode 3, integer 1-5 ratings from a
+planted rank-10 teacher, 90/10 split, J = R = 10, M = 65,536 -- generated
+synthetically (paper_2012_03550_b200/synth.py); Netflix itself is not here.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the unmodified reference sources compiled in place; else the C oracle port) on
+a bounded sample of the same workload with every host thread.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+CPU_SAMPLE_NNZ = 3_000_000
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
+    p.add_argument("--scale", type=float, default=1.0,
+                   help="fraction of the config's nnz (debug only; 1.0 for reported runs)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_NNZ)
+    return p.parse_args()
+
+
+HYPER = dict(lr_a=0.01, lr_b=0.01, reg_a=0.01, reg_b=0.01, init_mean=0.5, init_sd=0.1, seed=1)
+BATCH_M = {2: 65536, 3: 262144, 4: 65536, 5: 262144}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        os.unlink(self.path)
+        rows = [[x.strip() for x in r] for r in rows if len(r) >= 7]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_data(cfg: int, scale: float, device):
+    import torch
+    from paper_2012_03550_b200 import synth
+    spec = synth.CONFIGS[cfg]
+    if scale != 1.0:
+        spec = synth.scaled(spec, scale ** (1.0 / len(spec.dims)), int(spec.nnz * scale))
+    t0 = time.time()
+    (trc, trv), (tec, tev), perms = synth.generate(spec, device)
+    torch.cuda.synchronize()
+    data = dict(
+        spec=spec,
+        train=(trc.cpu().numpy().astype(np.uint32), trv.cpu().numpy()),
+        test=(tec.cpu().numpy().astype(np.uint32), tev.cpu().numpy()),
+        perms=[p.cpu().numpy().astype(np.uint32) for p in perms],
+        gen_s=time.time() - t0,
+    )
+    del trc, trv, tec, tev, perms
+    torch.cuda.empty_cache()
+    return data
+
+
+def units_per_epoch(order, m, nnz):
+    return order * (m + nnz)
+
+
+def bytes_per_unit(order, R):
+    """B_u = 4(N+1) + 4(N-1)R: one u32/fp32 COO record + N-1 gathered rows of R fp32."""
+    return 4 * (order + 1) + 4 * (order - 1) * R
+
+
+def init_model(dims, J, R, mean, sd, seed):
+    rs = np.random.default_rng(seed)
+    B = [rs.normal(mean, sd, (J, R)) for _ in dims]
+    A = [rs.normal(mean, sd, (d, J)) for d in dims]
+    return A, B
+
+
+def cpu_reference_run(data, J, R, m, warmup, epochs, threads):
+    """Reference CPU epochs on a bounded sample of the same tensor.
+    Returns (seconds/epoch, kind, cores, sample_desc, units/epoch)."""
+    from oracle import oracle_py as O
+    spec = data["spec"]
+    trc, trv = data["train"]
+    rs = np.random.default_rng(12345)
+    S = min(len(trv), data.get("cpu_sample", CPU_SAMPLE_NNZ))
+    pick = np.sort(rs.choice(len(trv), S, replace=False))
+    c, v = trc[pick], trv[pick]
+    order = len(spec.dims)
+    mm = min(m, S)
+    Jv = np.array([J] * order, np.uint32)
+    desc = (f"{S:,} of {len(trv):,} training nonzeros of config {data['cfg']} (uniform random "
+            f"subset, same shape), M={mm}, {epochs} timed epoch(s) after {warmup} warm-up, "
+            f"Strategy::Improved, init N(0.5,0.1^2)")
+    if O.ref_available():
+        import ctypes as C
+        t = O.RefTensor(spec.dims, c, v)
+        sec = C.c_double()
+        rc = O.ref().ref_bench_epoch_seconds(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"],
+                                            mm, 2, threads, warmup, epochs, 1, C.byref(sec))
+        if rc != 0:
+            raise RuntimeError(f"reference bench failed: {rc}")
+        return sec.value, "reference", threads, desc, units_per_epoch(order, mm, S)
+    # oracle port: single thread, serial strategy
+    t = O.Tensor(spec.dims, c, v)
+    model = O.Model(spec.dims, Jv, R).init_gaussian(0.5, 0.1, 1)
+    rng = O.Rng(2)
+    ws = O.CoreWorkspace(S)
+    times = []
+    for e in range(warmup + epochs):
+        t0 = time.perf_counter()
+        O.update_core_epoch(model, t, HYPER["lr_b"], HYPER["reg_b"], mm, rng, ws)
+        O.update_factor_epoch(model, t, HYPER["lr_a"], HYPER["reg_a"], rng)
+        if e >= warmup:
+            times.append(time.perf_counter() - t0)
+    return statistics.median(times), "port", 1, desc.replace("Strategy::Improved", "serial C port"), \
+        units_per_epoch(order, mm, S)
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    import torch
+    cfg = args.config
+    data = make_data(cfg, args.scale, "cuda" if torch.cuda.is_available() else "cpu")
+    data["cfg"] = cfg
+    data["cpu_sample"] = args.cpu_sample
+    spec = data["spec"]
+    threads = os.cpu_count() or 1
+    J = R = spec.teacher_j
+    m = BATCH_M[cfg]
+    sec, kind, cores, desc, units = cpu_reference_run(data, J, R, m, args.warmup, args.steps, threads)
+    value = units / sec
+    line = {
+        "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "gpu_launches": 0,
+        "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz": spec.nnz, "J": J, "R": R,
+                   "batch_m": m, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind, "sample": desc},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2012_03550_b200 import sgdt
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = args.config
+    data = make_data(cfg, args.scale, torch.device("cuda", local_rank))
+    data["cfg"] = cfg
+    data["cpu_sample"] = args.cpu_sample
+    spec = data["spec"]
+    order = len(spec.dims)
+    J = R = spec.teacher_j
+    m = BATCH_M[cfg]
+    trc, trv = data["train"]
+    nnz = len(trv)
+
+    t0 = time.time()
+    s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"], perms=data["perms"],
+                     device=local_rank)
+    setup_s = time.time() - t0
+    A, B = init_model(spec.dims, J, R, HYPER["init_mean"], HYPER["init_sd"], HYPER["seed"])
+    s.set_model(A, B)
+    s.seed(HYPER["seed"] + 1)
+    ch = sgdt.CoreHyper(HYPER["lr_b"], HYPER["reg_b"], m, 0, 0)
+    fh = sgdt.FactorHyper(HYPER["lr_a"], HYPER["reg_a"], 1.0)
+    for _ in range(args.warmup):
+        s.run_epochs(ch, fh, 1)
+
+    stream = torch.cuda.ExternalStream(s.stream)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = s.launch_count()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        s.run_epochs(ch, fh, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = s.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    timing = s.last_timing()
+    units = units_per_epoch(order, m, nnz)
+    value = units * args.steps * world / (elapsed_ms * 1e-3)
+    ms_per_step = elapsed_ms / args.steps
+
+    # roofline of the dominant kernel (factor phase, one launch per mode)
+    bu = bytes_per_unit(order, R)
+    mode_ms = [timing.factor_mode_ms[n] for n in range(order)]
+    avg_mode_ms = sum(mode_ms) / order
+    achieved_gbs = nnz * bu / (avg_mode_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "factor_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"config{cfg}")
+        except Exception:
+            traffic = None
+
+    rmse = s.eval(1)[0]
+
+    # end to end through the C-ABI with host buffers: H2D model, epoch, D2H model
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        hA, hB = [pin(a) for a in A], [pin(b) for b in B]
+        oA = [torch.empty(a.shape, dtype=torch.float64).pin_memory().numpy() for a in A]
+        oB = [torch.empty(b.shape, dtype=torch.float64).pin_memory().numpy() for b in B]
+        s.get_model((hA, hB))  # continue from the trained state
+        h2d = sum(a.nbytes for a in hA) + sum(b.nbytes for b in hB)
+        d2h = sum(a.nbytes for a in oA) + sum(b.nbytes for b in oB)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.set_model(hA, hB)
+            s.run_epochs(ch, fh, 1)
+            s.get_model((oA, oB))
+            hA, oA = oA, hA
+            hB, oB = oB, hB
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": units * world / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "sgdt_set_model (fp64 pinned host) + sgdt_run_epochs(1) + sgdt_get_model (fp64 pinned host)",
+               "setup_s": setup_s}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            sec, kind, cores, desc, cu = cpu_reference_run(data, J, R, m, 1, 1, os.cpu_count() or 1)
+            cpu = {"value": cu / sec, "unit": "updates/s", "cores": cores, "kind": kind, "sample": desc}
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"{type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
+            "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz_total": spec.nnz,
+                       "nnz_train": nnz, "J": J, "R": R, "batch_m": m, "units_per_step": units,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "COO record copies (4 x 16 B x nnz) exceed the 126 MB L2; Q tables are L2-resident by design",
+                       "test_rmse_after": rmse, "data_gen_s": data["gen_s"], "setup_s": setup_s},
+            "phase_ms": {"core": timing.core_ms, "factor": timing.factor_ms, "factor_modes": mode_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "traffic": traffic,
+                         "kernel": "factor_chunk_kernel + factor_split_kernel (one mode)",
+                         "bytes_per_unit": bu, "units_per_launch": nnz, "peak_source": peak_src},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -155,6 +155,9 @@ int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyp
 
 int sgdt_last_timing(sgdt_session* s, sgdt_timing* t);
 
+/* Number of kernels this session has launched so far (all sgdt_* kernels). */
+uint64_t sgdt_launch_count(sgdt_session* s);
+
 /* Device next_below over an explicit MT state (test hook for the rejection
  * path, rng.hpp:20-25): draws n values with bounds[i] sequentially. */
 int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,

@@ -261,6 +261,7 @@ int core_launch_rp(Session& s, CoreArgs& a) {
   void* args[] = {&a};
   SGDT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(block),
                                         args, smem, s.stream));
+  ++s.launches;
   return SGDT_OK;
 }
 
@@ -271,6 +272,7 @@ int q_launch_rp(Session& s, int k) {
   if (blocks > static_cast<uint64_t>(s.num_sms) * 8) blocks = s.num_sms * 8;
   q_refresh_kernel<RP><<<static_cast<unsigned>(blocks), 256, smem, s.stream>>>(s.P, k);
   SGDT_CUDA(cudaGetLastError());
+  ++s.launches;
   return SGDT_OK;
 }
 

@@ -102,6 +102,7 @@ int launch_eval(Session& s, int which, double* rmse, double* mae) {
   if (r) return r;
   eval_final_kernel<<<1, 32, 0, s.stream>>>(s.ev_part, nblocks, rc.nnz, s.ev_out);
   SGDT_CUDA(cudaGetLastError());
+  s.launches += 2;
   SGDT_CUDA(cudaMemcpyAsync(s.h_ev_out, s.ev_out, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             s.stream));
   SGDT_CUDA(cudaStreamSynchronize(s.stream));

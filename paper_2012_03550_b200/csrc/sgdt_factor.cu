@@ -253,11 +253,13 @@ int factor_launch_rp(Session& s, FactorArgs& a) {
     const unsigned grid = (a.n_chunks + wpb - 1) / wpb;
     factor_chunk_kernel<RP><<<grid, block, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
+    ++s.launches;
   }
   if (a.n_splits) {
     const unsigned grid = (a.n_splits + wpb - 1) / wpb;
     factor_split_kernel<RP><<<grid, block, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
+    ++s.launches;
   }
   return SGDT_OK;
 }

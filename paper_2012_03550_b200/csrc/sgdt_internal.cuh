@@ -127,6 +127,7 @@ struct Session {
   cudaEvent_t ev[4 + kMaxOrder] = {};
   sgdt_timing timing{};
   bool timing_valid = false;
+  uint64_t launches = 0;  // kernels launched by this session
 };
 
 // error plumbing (sgdt_session.cu)

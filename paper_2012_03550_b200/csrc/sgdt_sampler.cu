@@ -202,6 +202,7 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch) {
   cudaStream_t st = s.stream;
   if (!s.pool_valid) {
     iota_kernel<<<s.num_sms * 4, 256, 0, st>>>(s.pool, s.nnz);
+    ++s.launches;
     SGDT_CUDA(cudaGetLastError());
     s.pool_valid = true;
   }
@@ -218,6 +219,7 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch) {
   write_pool_kernel<<<blocks, 256, 0, st>>>(m, s.pool, s.draw_j, s.head, s.link, s.stamp,
                                             out_batch, s.dval);
   SGDT_CUDA(cudaGetLastError());
+  s.launches += 5;
   s.last_batch = out_batch;
   s.last_batch_len = m;
   return SGDT_OK;

@@ -333,6 +333,7 @@ int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m) {
   if (h.batch_m == 0) {
     iota32_kernel<<<grid_for(m, s.num_sms), 256, 0, s.stream>>>(s.batch, m);
     SGDT_CUDA(cudaGetLastError());
+    ++s.launches;
     s.last_batch = s.batch;
     s.last_batch_len = m;
   } else {
@@ -538,6 +539,7 @@ int sgdt_set_model(sgdt_session* s, const double* const* A, const double* const*
     SGDT_CUDA(cudaMemcpyAsync(s->stage, B[k], nb * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     cast_d2f_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->stage, s->P.B[k], nb);
     SGDT_CUDA(cudaGetLastError());
+    s->launches += 2;
   }
   for (int k = 0; k < s->order; ++k) TRY(launch_q_refresh(*s, k));
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
@@ -555,6 +557,7 @@ int sgdt_get_model(sgdt_session* s, double* const* A, double* const* B) {
     cast_f2d_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->P.B[k], s->stage, nb);
     SGDT_CUDA(cudaMemcpyAsync(B[k], s->stage, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     SGDT_CUDA(cudaGetLastError());
+    s->launches += 2;
   }
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
   return SGDT_OK;
@@ -698,6 +701,8 @@ int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyp
   }
   return SGDT_OK;
 }
+
+uint64_t sgdt_launch_count(sgdt_session* s) { return s ? s->launches : 0; }
 
 int sgdt_last_timing(sgdt_session* s, sgdt_timing* t) {
   if (!s || !t) return fail(SGDT_ERR_DOMAIN, "null argument");

@@ -120,6 +120,8 @@ def load(build_if_missing: bool = True):
     L.sgdt_train.argtypes = [vp, C.POINTER(CoreHyper), C.POINTER(FactorHyper), C.c_uint64,
                              C.POINTER(C.c_double)]
     L.sgdt_last_timing.argtypes = [vp, C.POINTER(Timing)]
+    L.sgdt_launch_count.argtypes = [vp]
+    L.sgdt_launch_count.restype = C.c_uint64
     L.sgdt_rng_next_below.argtypes = [u64p, C.c_uint32, u64p, C.c_uint64, u64p, u64p, u32p]
     L.sgdt_partition_even.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p]
     _lib = L
@@ -294,6 +296,9 @@ class Session:
         out = np.zeros(epochs * 6)
         _ck(_lib.sgdt_train(self.h, C.byref(core), C.byref(factor), epochs, _p(out, C.c_double)))
         return out.reshape(epochs, 6)
+
+    def launch_count(self) -> int:
+        return int(_lib.sgdt_launch_count(self.h))
 
     def last_timing(self) -> Timing:
         t = Timing()
