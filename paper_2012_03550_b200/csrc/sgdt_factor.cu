@@ -35,8 +35,10 @@ constexpr unsigned kFull = 0xffffffffu;
 struct FactorArgs {
   Params P;
   int n;
-  const uint32_t* idx;  // mode-n copy: order x nnz (0-based)
-  const float* val;     // nnz
+  const uint32_t* keys;                  // mode-n coordinates of the mode-n copy
+  const float* val;                      // nnz
+  const uint32_t* oidx[kMaxOrder - 1];   // other modes' coordinates (mode-n copy)
+  const float* oq[kMaxOrder - 1];        // other modes' Q tables
   uint64_t nnz;
   const uint32_t* row_ptr;
   const Chunk* chunks;
@@ -58,9 +60,8 @@ __device__ __forceinline__ void load_bsn(const FactorArgs& a, float* bsn) {
 }
 
 // F = B^(n) g; a -= lr (F/cnt + reg a); Q^(n)[row] = a B^(n).  One lane.
-template <int RP>
-__device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row,
-                             const double (&g)[RP]) {
+template <int RP, typename T>
+__device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row, const T (&g)[RP]) {
   const uint32_t jn = a.P.J[a.n];
   const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
   const double inv = 1.0 / static_cast<double>(cnt);
@@ -72,7 +73,8 @@ __device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row
   for (uint32_t j = 0; j < jn; ++j) {
     double F = 0.0;
 #pragma unroll
-    for (int r = 0; r < RP; ++r) F = fma(static_cast<double>(bsn[j * RP + r]), g[r], F);
+    for (int r = 0; r < RP; ++r)
+      F = fma(static_cast<double>(bsn[j * RP + r]), static_cast<double>(g[r]), F);
     double w = static_cast<double>(arow[j]);
     bad |= !isfinite(w) || !isfinite(F);
     w -= a.lr * (F * inv + a.reg * w);
@@ -88,11 +90,11 @@ __device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row
   if (bad) atomicOr(a.flag, 8);
 }
 
-template <int RP>
-__device__ __forceinline__ void warp_allreduce(double (&x)[RP]) {
+template <int RP, typename T>
+__device__ __forceinline__ void warp_allreduce(T (&x)[RP]) {
 #pragma unroll
   for (int r = 0; r < RP; ++r) {
-    double v = x[r];
+    T v = x[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     x[r] = v;
@@ -100,7 +102,17 @@ __device__ __forceinline__ void warp_allreduce(double (&x)[RP]) {
 }
 
 template <int RP>
-__global__ void __launch_bounds__(256) factor_chunk_kernel(FactorArgs a) {
+constexpr int factor_min_blocks() {
+  return RP <= 4 ? 4 : (RP <= 12 ? 3 : 2);
+}
+
+// One warp streams one chunk of the mode-n-sorted records (see file header).
+// The next window's records are prefetched while the current window's Q rows
+// are gathered; per-lane partial sums stay in fp32 (a chunk holds at most
+// chunk_size entries, i.e. <= chunk_size/32 terms per lane) and are widened
+// to fp64 at every row boundary.
+template <int RP, int NO>
+__global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
   __shared__ float bsn[SGDT_MAX_J * RP];
   load_bsn<RP>(a, bsn);
   __syncthreads();
@@ -108,72 +120,99 @@ __global__ void __launch_bounds__(256) factor_chunk_kernel(FactorArgs a) {
   const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= a.n_chunks) return;
   const Chunk ch = a.chunks[wid];
-  const int n = a.n, order = a.P.order;
-  const uint32_t* keys = a.idx + static_cast<uint64_t>(n) * a.nnz;
-  const float* Qn = a.P.Q[n];
+  const float* Qn = a.P.Q[a.n];
 
-  uint32_t cur = keys[ch.begin];
-  double acc[RP];
+  // software pipeline: records of the next window
+  uint32_t pk = kNone, pi[NO];
+  float px = 0.f;
+  {
+    const uint32_t e = ch.begin + lane;
+    if (e < ch.end) {
+      pk = __ldcs(a.keys + e);
+      px = __ldcs(a.val + e);
 #pragma unroll
-  for (int r = 0; r < RP; ++r) acc[r] = 0.0;
-  bool spread = false;   // acc spread over all lanes (else only in carry_lane)
+      for (int j = 0; j < NO; ++j) pi[j] = __ldcs(a.oidx[j] + e);
+    }
+  }
+  uint32_t cur = __shfl_sync(kFull, pk, 0);
+  float acc[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) acc[r] = 0.f;
+  bool spread = false;  // acc spread over all lanes (else it lives in carry_lane)
   int carry_lane = 0;
 
   for (uint32_t base = ch.begin; base < ch.end; base += 32) {
-    const uint32_t e = base + lane;
-    const bool valid = e < ch.end;
-    uint32_t key = kNone;
+    const uint32_t key = pk;
+    const float x = px;
+    uint32_t ik[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) ik[j] = pi[j];
+    const bool valid = key != kNone;
+    {
+      const uint32_t e = base + 32 + lane;
+      pk = kNone;
+      if (e < ch.end) {
+        pk = __ldcs(a.keys + e);
+        px = __ldcs(a.val + e);
+#pragma unroll
+        for (int j = 0; j < NO; ++j) pi[j] = __ldcs(a.oidx[j] + e);
+      }
+    }
     float v[RP];
-#pragma unroll
-    for (int r = 0; r < RP; ++r) v[r] = 0.f;
     if (valid) {
-      key = __ldcs(keys + e);
-      const float x = __ldcs(a.val + e);
-      float c[RP];
+      float4 g[NO][RP / 4];
 #pragma unroll
-      for (int r = 0; r < RP; ++r) c[r] = 1.f;
-      for (int k = 0; k < order; ++k) {
-        if (k == n) continue;
-        const uint32_t ik = __ldcs(a.idx + static_cast<uint64_t>(k) * a.nnz + e);
-        const float4* qk = reinterpret_cast<const float4*>(a.P.Q[k] + static_cast<uint64_t>(ik) * RP);
+      for (int j = 0; j < NO; ++j) {
+        const float4* qk = reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP);
 #pragma unroll
-        for (int r = 0; r < RP; r += 4) {
-          const float4 t = __ldg(qk + r / 4);
-          c[r] *= t.x;
-          c[r + 1] *= t.y;
-          c[r + 2] *= t.z;
-          c[r + 3] *= t.w;
-        }
+        for (int r = 0; r < RP / 4; ++r) g[j][r] = __ldg(qk + r);
       }
       const float4* qn = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP);
+      float4 h[RP / 4];
+#pragma unroll
+      for (int r = 0; r < RP / 4; ++r) h[r] = qn[r];
       float p = 0.f;
 #pragma unroll
-      for (int r = 0; r < RP; r += 4) {
-        const float4 t = qn[r / 4];
-        p = fmaf(t.x, c[r], p);
-        p = fmaf(t.y, c[r + 1], p);
-        p = fmaf(t.z, c[r + 2], p);
-        p = fmaf(t.w, c[r + 3], p);
+      for (int r = 0; r < RP / 4; ++r) {
+        float4 c = g[0][r];
+#pragma unroll
+        for (int j = 1; j < NO; ++j) {
+          c.x *= g[j][r].x;
+          c.y *= g[j][r].y;
+          c.z *= g[j][r].z;
+          c.w *= g[j][r].w;
+        }
+        v[4 * r] = c.x;
+        v[4 * r + 1] = c.y;
+        v[4 * r + 2] = c.z;
+        v[4 * r + 3] = c.w;
+        p = fmaf(h[r].x, c.x, p);
+        p = fmaf(h[r].y, c.y, p);
+        p = fmaf(h[r].z, c.z, p);
+        p = fmaf(h[r].w, c.w, p);
       }
       const float t = p - x;
 #pragma unroll
-      for (int r = 0; r < RP; ++r) v[r] = t * c[r];
+      for (int r = 0; r < RP; ++r) v[r] *= t;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) v[r] = 0.f;
     }
     if (__all_sync(kFull, key == cur)) {
 #pragma unroll
-      for (int r = 0; r < RP; ++r) acc[r] += static_cast<double>(v[r]);
+      for (int r = 0; r < RP; ++r) acc[r] += v[r];
       spread = true;
       continue;
     }
     // ---- window crosses a row boundary
-    double tot[RP];
-    if (spread) {
+    float tot[RP];
 #pragma unroll
-      for (int r = 0; r < RP; ++r) tot[r] = acc[r];
+    for (int r = 0; r < RP; ++r) tot[r] = acc[r];
+    if (spread) {
       warp_allreduce<RP>(tot);
     } else {
 #pragma unroll
-      for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, acc[r], carry_lane);
+      for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, tot[r], carry_lane);
     }
     // segmented inclusive scan of v by key (keys are sorted inside the window)
 #pragma unroll
@@ -192,26 +231,27 @@ __global__ void __launch_bounds__(256) factor_chunk_kernel(FactorArgs a) {
     const bool seg_end = valid && (lane == 31 || nkey != key);
     const bool is_last = static_cast<int>(lane) == last_valid;
     const bool first_seg = key == cur;
-    double g[RP];
+    if (first_seg) {
 #pragma unroll
-    for (int r = 0; r < RP; ++r) g[r] = static_cast<double>(v[r]) + (first_seg ? tot[r] : 0.0);
+      for (int r = 0; r < RP; ++r) v[r] += tot[r];
+    }
     if (lane == 0 && key != cur) finalize_row<RP>(a, bsn, cur, tot);  // row ended at the window edge
-    if (seg_end && !is_last) finalize_row<RP>(a, bsn, key, g);
+    if (seg_end && !is_last) finalize_row<RP>(a, bsn, key, v);
     cur = __shfl_sync(kFull, key, last_valid);
 #pragma unroll
-    for (int r = 0; r < RP; ++r) acc[r] = is_last ? g[r] : 0.0;
+    for (int r = 0; r < RP; ++r) acc[r] = is_last ? v[r] : 0.f;
     spread = false;
     carry_lane = last_valid;
   }
   // ---- the open row at the chunk end
-  double tot[RP];
-  if (spread) {
+  float tot[RP];
 #pragma unroll
-    for (int r = 0; r < RP; ++r) tot[r] = acc[r];
+  for (int r = 0; r < RP; ++r) tot[r] = acc[r];
+  if (spread) {
     warp_allreduce<RP>(tot);
   } else {
 #pragma unroll
-    for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, acc[r], carry_lane);
+    for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, tot[r], carry_lane);
   }
   if (lane == 0) {
     if (ch.piece < 0) {
@@ -219,7 +259,7 @@ __global__ void __launch_bounds__(256) factor_chunk_kernel(FactorArgs a) {
     } else {
       double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
 #pragma unroll
-      for (int r = 0; r < RP; ++r) dst[r] = tot[r];
+      for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(tot[r]);
     }
   }
 }
@@ -246,12 +286,12 @@ __global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
   if (lane == 0) finalize_row<RP>(a, bsn, sr.row, g);
 }
 
-template <int RP>
-int factor_launch_rp(Session& s, FactorArgs& a) {
+template <int RP, int NO>
+int factor_launch(Session& s, FactorArgs& a) {
   const int block = 256, wpb = block / 32;
   if (a.n_chunks) {
     const unsigned grid = (a.n_chunks + wpb - 1) / wpb;
-    factor_chunk_kernel<RP><<<grid, block, 0, s.stream>>>(a);
+    factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
     ++s.launches;
   }
@@ -264,6 +304,22 @@ int factor_launch_rp(Session& s, FactorArgs& a) {
   return SGDT_OK;
 }
 
+template <int NO>
+int factor_launch_no(Session& s, FactorArgs& a) {
+  switch (s.RP) {
+    case 4: return factor_launch<4, NO>(s, a);
+    case 8: return factor_launch<8, NO>(s, a);
+    case 12: return factor_launch<12, NO>(s, a);
+    case 16: return factor_launch<16, NO>(s, a);
+    case 20: return factor_launch<20, NO>(s, a);
+    case 24: return factor_launch<24, NO>(s, a);
+    case 28: return factor_launch<28, NO>(s, a);
+    case 32: return factor_launch<32, NO>(s, a);
+    default: break;
+  }
+  return fail(SGDT_ERR_CONFIG, "unsupported R_core");
+}
+
 }  // namespace
 
 int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
@@ -271,8 +327,15 @@ int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
   FactorArgs a{};
   a.P = s.P;
   a.n = n;
-  a.idx = mp.rec.idx;
+  a.keys = mp.rec.idx + static_cast<uint64_t>(n) * mp.rec.nnz;
   a.val = mp.rec.val;
+  int j = 0;
+  for (int k = 0; k < s.order; ++k) {
+    if (k == n) continue;
+    a.oidx[j] = mp.rec.idx + static_cast<uint64_t>(k) * mp.rec.nnz;
+    a.oq[j] = s.P.Q[k];
+    ++j;
+  }
   a.nnz = mp.rec.nnz;
   a.row_ptr = mp.row_ptr;
   a.chunks = mp.chunks;
@@ -283,18 +346,17 @@ int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;
-  switch (s.RP) {
-    case 4: return factor_launch_rp<4>(s, a);
-    case 8: return factor_launch_rp<8>(s, a);
-    case 12: return factor_launch_rp<12>(s, a);
-    case 16: return factor_launch_rp<16>(s, a);
-    case 20: return factor_launch_rp<20>(s, a);
-    case 24: return factor_launch_rp<24>(s, a);
-    case 28: return factor_launch_rp<28>(s, a);
-    case 32: return factor_launch_rp<32>(s, a);
+  switch (s.order - 1) {
+    case 1: return factor_launch_no<1>(s, a);
+    case 2: return factor_launch_no<2>(s, a);
+    case 3: return factor_launch_no<3>(s, a);
+    case 4: return factor_launch_no<4>(s, a);
+    case 5: return factor_launch_no<5>(s, a);
+    case 6: return factor_launch_no<6>(s, a);
+    case 7: return factor_launch_no<7>(s, a);
     default: break;
   }
-  return fail(SGDT_ERR_CONFIG, "unsupported R_core");
+  return fail(SGDT_ERR_CONFIG, "unsupported tensor order");
 }
 
 }  // namespace sgdt
