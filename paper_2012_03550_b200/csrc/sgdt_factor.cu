@@ -59,35 +59,69 @@ __device__ __forceinline__ void load_bsn(const FactorArgs& a, float* bsn) {
   }
 }
 
-// F = B^(n) g; a -= lr (F/cnt + reg a); Q^(n)[row] = a B^(n).  One lane.
-template <int RP, typename T>
-__device__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row, const T (&g)[RP]) {
-  const uint32_t jn = a.P.J[a.n];
-  const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
-  const double inv = 1.0 / static_cast<double>(cnt);
-  float* arow = a.P.A[a.n] + static_cast<uint64_t>(row) * jn;
+// What a row update needs, small enough to pass by value to the out-of-line
+// finaliser (keeps the finaliser's registers out of the streaming loop).
+struct RowUpdate {
+  float* A;                 // A^(n)
+  float* Q;                 // Q^(n)
+  const uint32_t* row_ptr;  // mode-n row offsets
+  const float* bsn;         // B^(n) in shared memory, J x RP
+  uint32_t jn;
+  float lr, reg;
+  int* flag;
+};
+
+// F = B^(n) g; a -= lr (F/cnt + reg a); Q^(n)[row] = a B^(n).  One lane, fp32
+// (the parameters are fp32 on the device and F is an R-term dot product of
+// an fp32 row sum).  Two passes keep only g live across the J loop.
+template <int RP>
+__device__ __noinline__ void finalize_row_impl(RowUpdate u, uint32_t row, const float* g) {
+  const uint32_t cnt = u.row_ptr[row + 1] - u.row_ptr[row];
+  const float inv = 1.0f / static_cast<float>(cnt);
+  float* arow = u.A + static_cast<uint64_t>(row) * u.jn;
+  float gr[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) gr[r] = g[r];
   int bad = 0;
-  float q[RP];
+  for (uint32_t j = 0; j < u.jn; ++j) {
+    float F = 0.f;
 #pragma unroll
-  for (int r = 0; r < RP; ++r) q[r] = 0.f;
-  for (uint32_t j = 0; j < jn; ++j) {
-    double F = 0.0;
-#pragma unroll
-    for (int r = 0; r < RP; ++r)
-      F = fma(static_cast<double>(bsn[j * RP + r]), static_cast<double>(g[r]), F);
-    double w = static_cast<double>(arow[j]);
+    for (int r = 0; r < RP; ++r) F = fmaf(u.bsn[j * RP + r], gr[r], F);
+    const float w = arow[j];
     bad |= !isfinite(w) || !isfinite(F);
-    w -= a.lr * (F * inv + a.reg * w);
-    const float wf = static_cast<float>(w);
-    bad |= !isfinite(wf);
-    arow[j] = wf;
-#pragma unroll
-    for (int r = 0; r < RP; ++r) q[r] = fmaf(wf, bsn[j * RP + r], q[r]);
+    const float wn = w - u.lr * fmaf(F, inv, u.reg * w);
+    bad |= !isfinite(wn);
+    arow[j] = wn;
   }
-  float4* dst = reinterpret_cast<float4*>(a.P.Q[a.n] + static_cast<uint64_t>(row) * RP);
+  float4* dst = reinterpret_cast<float4*>(u.Q + static_cast<uint64_t>(row) * RP);
+#pragma unroll 1
+  for (int s = 0; s < RP / 4; ++s) {
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t j = 0; j < u.jn; ++j) {
+      const float wf = arow[j];
+      const float* b = u.bsn + j * RP + 4 * s;
+      q.x = fmaf(wf, b[0], q.x);
+      q.y = fmaf(wf, b[1], q.y);
+      q.z = fmaf(wf, b[2], q.z);
+      q.w = fmaf(wf, b[3], q.w);
+    }
+    dst[s] = q;
+  }
+  if (bad) atomicOr(u.flag, 8);
+}
+
+__device__ __forceinline__ RowUpdate row_update(const FactorArgs& a, const float* bsn) {
+  return RowUpdate{a.P.A[a.n], a.P.Q[a.n], a.row_ptr, bsn, a.P.J[a.n], static_cast<float>(a.lr),
+                   static_cast<float>(a.reg), a.flag};
+}
+
+template <int RP, typename T>
+__device__ __forceinline__ void finalize_row(const FactorArgs& a, const float* bsn, uint32_t row,
+                                             const T (&g)[RP]) {
+  float gf[RP];
 #pragma unroll
-  for (int r = 0; r < RP; r += 4) dst[r / 4] = make_float4(q[r], q[r + 1], q[r + 2], q[r + 3]);
-  if (bad) atomicOr(a.flag, 8);
+  for (int r = 0; r < RP; ++r) gf[r] = static_cast<float>(g[r]);
+  finalize_row_impl<RP>(row_update(a, bsn), row, gf);
 }
 
 template <int RP, typename T>

@@ -82,7 +82,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """libsgdt.so in-tree; SGDT_LIB overrides it (A/B builds of the same ABI)."""
+    return os.environ.get("SGDT_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -90,11 +91,12 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.LIB):
-        if not build_if_missing:
-            raise ImportError(f"{_build.LIB} is missing; run __graft_entry__.build()")
+    path = lib_path()
+    if not os.path.exists(path):
+        if not build_if_missing or path != _build.LIB:
+            raise ImportError(f"{path} is missing; run __graft_entry__.build()")
         _build.build()
-    L = C.CDLL(_build.LIB)
+    L = C.CDLL(path)
     vp = C.c_void_p
     u32p = C.POINTER(C.c_uint32)
     u64p = C.POINTER(C.c_uint64)
