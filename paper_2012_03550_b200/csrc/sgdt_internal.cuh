@@ -75,6 +75,8 @@ struct Session {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // sampler run-ahead (Psi does not depend on the model)
+  cudaEvent_t ev_start = nullptr, ev_core = nullptr, ev_samp = nullptr;
   int order = 0;
   uint32_t dims[kMaxOrder] = {};
   uint32_t J[kMaxOrder] = {};
@@ -99,7 +101,7 @@ struct Session {
   uint32_t* kprev = nullptr;    // m
   uint32_t* lprev = nullptr;    // m
   uint32_t* dval = nullptr;     // m
-  uint32_t* batch = nullptr;    // up to order x m (one Psi per mode when resampling)
+  uint32_t* batch = nullptr;    // 2 x order x m: double-buffered Psi (one per mode when resampling)
   uint64_t batch_cap = 0;
   uint64_t last_batch_len = 0;
   uint32_t* last_batch = nullptr;  // points into batch
@@ -145,7 +147,7 @@ int fail(int code, const std::string& msg);
   } while (0)
 
 // kernels (launchers return cudaError_t)
-int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch);
+int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st);
 int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, uint64_t m,
                 int per_mode_batches);
 int launch_q_refresh(Session& s, int mode);

@@ -198,8 +198,7 @@ __global__ void write_pool_kernel(uint64_t m, uint32_t* pool, const uint32_t* __
 
 }  // namespace
 
-int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch) {
-  cudaStream_t st = s.stream;
+int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st) {
   if (!s.pool_valid) {
     iota_kernel<<<s.num_sms * 4, 256, 0, st>>>(s.pool, s.nnz);
     ++s.launches;

@@ -252,14 +252,18 @@ void free_session(sgdt_session* s) {
   if (s->h_flag) cudaFreeHost(s->h_flag);
   for (auto& e : s->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {s->ev_start, s->ev_core, s->ev_samp})
+    if (e) cudaEventDestroy(e);
+  if (s->side) cudaStreamDestroy(s->side);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
 
 int ensure_batch_capacity(Session& s, uint64_t m) {
-  const uint64_t need = m * s.order;
+  const uint64_t need = 2 * m * s.order;
   if (need <= s.batch_cap) return SGDT_OK;
   SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  SGDT_CUDA(cudaStreamSynchronize(s.side));
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -284,6 +288,7 @@ int ensure_batch_capacity(Session& s, uint64_t m) {
 int ensure_core_capacity(Session& s, uint64_t m) {
   if (m <= s.cs_cap) return SGDT_OK;
   SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  SGDT_CUDA(cudaStreamSynchronize(s.side));
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -324,23 +329,34 @@ int check_factor_hyper(const sgdt_factor_hyper* h) {
   return SGDT_OK;
 }
 
-// Enqueue one core phase (no host sync).
-int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m) {
+// Draw the Psi of one epoch (one per mode when resampling) into `buf`.
+int enqueue_sample(Session& s, const sgdt_core_hyper& h, uint64_t m, uint32_t* buf, cudaStream_t st) {
+  const int draws = (h.resample_per_mode && h.batch_m != 0) ? s.order : 1;
+  for (int n = 0; n < draws; ++n) TRY(launch_sampler(s, m, buf + static_cast<uint64_t>(n) * m, st));
+  return SGDT_OK;
+}
+
+// Enqueue one core phase (no host sync).  `presampled` != nullptr: Psi was
+// already drawn (run-ahead on the side stream) into that buffer.
+int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_t* presampled = nullptr) {
   if (h.lr == 0.0) return SGDT_OK;  // frozen phase: bit-exact no-op, no RNG
   TRY(ensure_batch_capacity(s, m));
   TRY(ensure_core_capacity(s, m));
   const bool per_mode = h.resample_per_mode && h.batch_m != 0;
-  if (h.batch_m == 0) {
-    iota32_kernel<<<grid_for(m, s.num_sms), 256, 0, s.stream>>>(s.batch, m);
-    SGDT_CUDA(cudaGetLastError());
-    ++s.launches;
-    s.last_batch = s.batch;
-    s.last_batch_len = m;
-  } else {
-    const int draws = per_mode ? s.order : 1;
-    for (int n = 0; n < draws; ++n) TRY(launch_sampler(s, m, s.batch + static_cast<uint64_t>(n) * m));
+  const uint32_t* batch = presampled;
+  if (!batch) {
+    if (h.batch_m == 0) {
+      iota32_kernel<<<grid_for(m, s.num_sms), 256, 0, s.stream>>>(s.batch, m);
+      SGDT_CUDA(cudaGetLastError());
+      ++s.launches;
+      s.last_batch = s.batch;
+      s.last_batch_len = m;
+    } else {
+      TRY(enqueue_sample(s, h, m, s.batch, s.stream));
+    }
+    batch = s.batch;
   }
-  return launch_core(s, h, s.batch, m, per_mode ? 1 : 0);
+  return launch_core(s, h, batch, m, per_mode ? 1 : 0);
 }
 
 int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
@@ -419,7 +435,10 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
   s->num_sms = prop.multiProcessorCount;
   int rc = [&]() -> int {
     SGDT_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    SGDT_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
     for (auto& e : s->ev) SGDT_CUDA(cudaEventCreate(&e));
+    for (cudaEvent_t* e : {&s->ev_start, &s->ev_core, &s->ev_samp})
+      SGDT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     if (const char* cs = std::getenv("SGDT_CHUNK_SIZE")) {
       const long v = std::strtol(cs, nullptr, 10);
       if (v >= 1 && v <= (1L << 24)) s->chunk_size = static_cast<uint32_t>(v);
@@ -597,7 +616,7 @@ int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
   if (m < 1 || m > s->nnz) return fail(SGDT_ERR_DOMAIN, "sample_batch: batch size out of range");
   SGDT_CUDA(cudaSetDevice(s->device));
   TRY(ensure_batch_capacity(*s, m));
-  TRY(launch_sampler(*s, m, s->batch));
+  TRY(launch_sampler(*s, m, s->batch, s->stream));
   if (out) SGDT_CUDA(cudaMemcpyAsync(out, s->batch, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
   return SGDT_OK;
@@ -651,27 +670,48 @@ int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
   TRY(check_core_hyper(*s, ch, &m));
   TRY(check_factor_hyper(fh));
   SGDT_CUDA(cudaSetDevice(s->device));
-  const bool timed = true;
+  if (epochs == 0) return SGDT_OK;
+  // Psi does not depend on the model, so epoch e+1's sampler runs on the side
+  // stream during epoch e's factor phase (double-buffered Psi).  The RNG
+  // stream is consumed in exactly the reference order: the factor phase draws
+  // nothing (row_fraction == 1).
+  const bool ahead = ch->lr > 0.0 && ch->batch_m != 0;
+  uint32_t* buf[2] = {nullptr, nullptr};
+  if (ahead) {
+    TRY(ensure_batch_capacity(*s, m));
+    TRY(ensure_core_capacity(*s, m));
+    buf[0] = s->batch;
+    buf[1] = s->batch + static_cast<uint64_t>(s->order) * m;
+    SGDT_CUDA(cudaEventRecord(s->ev_start, s->stream));
+    SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_start, 0));
+    TRY(enqueue_sample(*s, *ch, m, buf[0], s->side));
+    SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+  }
   for (uint64_t e = 0; e < epochs; ++e) {
     const bool last = e + 1 == epochs;
-    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[0], s->stream));
-    TRY(enqueue_core(*s, *ch, m));
-    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[1], s->stream));
-    TRY(enqueue_factor(*s, *fh, last && timed));
-    if (last && timed) SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
+    if (ahead) SGDT_CUDA(cudaStreamWaitEvent(s->stream, s->ev_samp, 0));
+    if (last) SGDT_CUDA(cudaEventRecord(s->ev[0], s->stream));
+    TRY(enqueue_core(*s, *ch, m, ahead ? buf[e & 1] : nullptr));
+    if (ahead && !last) {
+      SGDT_CUDA(cudaEventRecord(s->ev_core, s->stream));
+      SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_core, 0));
+      TRY(enqueue_sample(*s, *ch, m, buf[(e + 1) & 1], s->side));
+      SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+    }
+    if (last) SGDT_CUDA(cudaEventRecord(s->ev[1], s->stream));
+    TRY(enqueue_factor(*s, *fh, last));
+    if (last) SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
   }
   TRY(sync_and_flag(*s));
-  if (epochs > 0) {
-    sgdt_timing t{};
-    SGDT_CUDA(cudaEventElapsedTime(&t.core_ms, s->ev[0], s->ev[1]));
-    SGDT_CUDA(cudaEventElapsedTime(&t.factor_ms, s->ev[1], s->ev[2]));
-    if (fh->lr > 0.0)
-      for (int n = 0; n < s->order; ++n)
-        SGDT_CUDA(cudaEventElapsedTime(&t.factor_mode_ms[n], s->ev[4 + n],
-                                       n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2]));
-    s->timing = t;
-    s->timing_valid = true;
-  }
+  sgdt_timing t{};
+  SGDT_CUDA(cudaEventElapsedTime(&t.core_ms, s->ev[0], s->ev[1]));
+  SGDT_CUDA(cudaEventElapsedTime(&t.factor_ms, s->ev[1], s->ev[2]));
+  if (fh->lr > 0.0)
+    for (int n = 0; n < s->order; ++n)
+      SGDT_CUDA(cudaEventElapsedTime(&t.factor_mode_ms[n], s->ev[4 + n],
+                                     n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2]));
+  s->timing = t;
+  s->timing_valid = true;
   return SGDT_OK;
 }
 

@@ -297,3 +297,32 @@ def test_run_to_run_bit_identical():
     for n in range(3):
         assert np.array_equal(outs[0][0][n], outs[1][0][n])
         assert np.array_equal(outs[0][1][n], outs[1][1][n])
+
+
+def test_run_epochs_pipelined_sampler_matches_oracle():
+    """sgdt_run_epochs draws epoch e+1's Psi on a side stream during epoch e's
+    factor phase; the RNG stream, the pool and every Psi must still be exactly
+    the reference's, and a short free run stays within the parity bar."""
+    dims, J, R = (40, 30, 20), (5, 5, 5), 5
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, R, 5000, 21, tm=0.0, ts=sig)
+    t = O.Tensor(dims, *tr)
+    for resample in (False, True):
+        s = session_for(dims, tr, J, R)
+        m = oracle_model(dims, J, R, 9, sd=sig, mean=0.0)
+        s.set_model(*m.params())
+        rng = O.Rng(8)
+        ws = O.CoreWorkspace(5000)
+        s.set_rng(*rng.state())
+        s.run_epochs(sg().CoreHyper(0.01, 0.01, 512, int(resample), 0), sg().FactorHyper(0.01, 0.01, 1.0), 3)
+        for _ in range(3):
+            O.update_core_epoch(m, t, 0.01, 0.01, 512, rng, ws, resample)
+            O.update_factor_epoch(m, t, 0.01, 0.01, rng)
+        assert np.array_equal(s.last_batch(), ws.batch())
+        st, pos = s.get_rng()
+        rst, rpos = rng.state()
+        assert pos == rpos and np.array_equal(st, rst)
+        A, B = s.get_model()
+        RA, RB = m.params()
+        for n in range(3):
+            assert rel_err(A[n], RA[n]) <= TOL and rel_err(B[n], RB[n]) <= TOL
