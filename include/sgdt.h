@@ -126,6 +126,11 @@ int sgdt_get_rng(sgdt_session* s, uint64_t* mt312, uint32_t* pos);
  * sized wrong, sptensor.cpp:260-263). */
 int sgdt_reset_pool(sgdt_session* s);
 
+/* The persistent sample pool (CoreBatchWorkspace::sample_pool,
+ * core_optimizer.hpp:36): nnz entry ids, a permutation of 0..nnz-1. */
+int sgdt_set_pool(sgdt_session* s, const uint32_t* pool);
+int sgdt_get_pool(sgdt_session* s, uint32_t* pool);
+
 /* sample_batch (sptensor.cpp:256-270) on the device pool; out (host, m
  * entries) may be NULL. */
 int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out);
@@ -154,6 +159,10 @@ int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyp
                uint64_t epochs, double* metrics);
 
 int sgdt_last_timing(sgdt_session* s, sgdt_timing* t);
+
+/* Device bytes held by the session's per-epoch scratch (the analogue of the
+ * workspace footprint the reference reports as peak_bytes, trainer.cpp:116-119). */
+uint64_t sgdt_workspace_bytes(sgdt_session* s);
 
 /* Number of kernels this session has launched so far (all sgdt_* kernels). */
 uint64_t sgdt_launch_count(sgdt_session* s);

@@ -1,0 +1,153 @@
+// sptensor.cpp -- host construction of CooTensor (validation + per-mode
+// buckets, the layout the device copies are built from) and the device-backed
+// sampler entry points.
+#include "sptucker/sptensor.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <string>
+
+#include "device.hpp"
+
+namespace sptucker {
+
+Shape::Shape(std::vector<std::uint32_t> dims) : dims_(std::move(dims)) {
+  if (dims_.size() < 2) throw DomainError("shape: order must be at least 2");
+  if (dims_.size() > SGDT_MAX_ORDER) throw DomainError("shape: order above 8 is not supported on the device");
+  // Deviation (documented in DESIGN.md): the reference rejects shapes whose
+  // element count overflows 64 bits (sptensor.cpp:34-35); nothing on the
+  // device path linearises coordinates, so such shapes are accepted and
+  // total_elems() saturates.
+  total_ = 1;
+  for (const std::uint32_t d : dims_) {
+    if (d < 1) throw DomainError("shape: every dim must be >= 1");
+    total_ = total_ > std::numeric_limits<std::uint64_t>::max() / d ? std::numeric_limits<std::uint64_t>::max()
+                                                                     : total_ * d;
+  }
+}
+
+namespace {
+
+// Duplicate detection: sort (128-bit) linear positions and look for equal
+// neighbours.  The linear key of the reference (mode 1 fastest) wraps for
+// shapes beyond 2^64 elements, hence the two-word key.
+bool has_duplicate(const Shape& shape, const std::vector<std::uint32_t>& coords, std::size_t nnz) {
+  const std::size_t order = shape.order();
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> keys(nnz);
+  for (std::size_t e = 0; e < nnz; ++e) {
+    unsigned __int128 key = 0, stride = 1;
+    for (std::size_t k = 0; k < order; ++k) {
+      key += static_cast<unsigned __int128>(coords[e * order + k] - 1) * stride;
+      stride *= shape.dim(k);
+    }
+    keys[e] = {static_cast<std::uint64_t>(key >> 64), static_cast<std::uint64_t>(key)};
+  }
+  std::sort(keys.begin(), keys.end());
+  return std::adjacent_find(keys.begin(), keys.end()) != keys.end();
+}
+
+}  // namespace
+
+CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector<double> values)
+    : shape_(std::move(shape)), coords_(std::move(coords)), values_(std::move(values)) {
+  const std::size_t order = shape_.order();
+  const std::size_t nnz = values_.size();
+  if (nnz == 0) throw DataError("tensor has no entries");
+  if (coords_.size() != nnz * order) throw DataError("coords/values length mismatch");
+  if (nnz > std::numeric_limits<std::uint32_t>::max()) throw DataError("entry count exceeds the 32-bit id space");
+  for (std::size_t e = 0; e < nnz; ++e)
+    for (std::size_t k = 0; k < order; ++k) {
+      const std::uint32_t c = coords_[e * order + k];
+      if (c < 1 || c > shape_.dim(k)) throw DataError("entry " + std::to_string(e) + ": coordinate out of range");
+    }
+  if (has_duplicate(shape_, coords_, nnz)) throw DataError("duplicate coordinate");
+
+  // Stable counting sort per mode: bucket i holds the entries with i_n = i in
+  // ascending entry id (the order the device mode copies inherit).
+  mode_perm_.assign(order, {});
+  mode_offsets_.assign(order, {});
+  for (std::size_t n = 0; n < order; ++n) {
+    std::vector<std::uint64_t>& off = mode_offsets_[n];
+    off.assign(static_cast<std::size_t>(shape_.dim(n)) + 1, 0);
+    for (std::size_t e = 0; e < nnz; ++e) ++off[coords_[e * order + n]];
+    std::partial_sum(off.begin(), off.end(), off.begin());
+    std::vector<std::uint64_t> next(off.begin(), off.end() - 1);
+    std::vector<std::uint32_t>& perm = mode_perm_[n];
+    perm.resize(nnz);
+    for (std::size_t e = 0; e < nnz; ++e) perm[next[coords_[e * order + n] - 1]++] = static_cast<std::uint32_t>(e);
+  }
+}
+
+double CooTensor::mean_value() const {
+  double s = 0.0;
+  for (const double v : values_) s += v;
+  return s / static_cast<double>(values_.size());
+}
+
+detail::DeviceCache& CooTensor::device_cache() const {
+  if (!device_) device_ = std::make_shared<detail::DeviceCache>();
+  return *device_;
+}
+
+std::pair<CooTensor, CooTensor> train_test_split(const CooTensor& t, double test_fraction, std::uint64_t seed) {
+  if (!(test_fraction > 0.0 && test_fraction < 1.0)) throw DomainError("train_test_split: fraction must lie in (0,1)");
+  const std::size_t nnz = t.nnz();
+  const std::size_t ntest = static_cast<std::size_t>(std::llround(test_fraction * static_cast<double>(nnz)));
+  if (ntest == 0 || ntest == nnz)
+    throw DomainError("train_test_split: degenerate split (|test|=" + std::to_string(ntest) + " of " +
+                      std::to_string(nnz) + ")");
+  std::vector<std::uint32_t> ids(nnz);
+  std::iota(ids.begin(), ids.end(), 0u);
+  Rng rng(seed);
+  for (std::size_t i = 0; i + 1 < nnz; ++i) std::swap(ids[i], ids[i + static_cast<std::size_t>(rng.next_below(nnz - i))]);
+  std::sort(ids.begin(), ids.begin() + static_cast<std::ptrdiff_t>(ntest));
+  std::sort(ids.begin() + static_cast<std::ptrdiff_t>(ntest), ids.end());
+  auto take = [&](std::size_t b, std::size_t e) {
+    std::vector<std::uint32_t> c;
+    std::vector<double> v;
+    c.reserve((e - b) * t.order());
+    v.reserve(e - b);
+    for (std::size_t i = b; i < e; ++i) {
+      const auto cc = t.coord(ids[i]);
+      c.insert(c.end(), cc.begin(), cc.end());
+      v.push_back(t.value(ids[i]));
+    }
+    return CooTensor(t.shape(), std::move(c), std::move(v));
+  };
+  CooTensor test = take(0, ntest);
+  CooTensor train = take(ntest, nnz);
+  return {std::move(train), std::move(test)};
+}
+
+namespace {
+detail::Session& sampler_session(const CooTensor& t) {
+  return detail::session_for(t, nullptr, t.shape(), Ranks{std::vector<std::uint32_t>(t.order(), 1), 1});
+}
+}  // namespace
+
+void sample_batch(const CooTensor& t, std::size_t m, Rng& rng, std::vector<std::uint32_t>& pool,
+                  std::vector<std::uint32_t>& out) {
+  const std::size_t nnz = t.nnz();
+  if (m < 1 || m > nnz) throw DomainError("sample_batch: batch size out of range");
+  if (pool.size() != nnz) {
+    pool.resize(nnz);
+    std::iota(pool.begin(), pool.end(), 0u);
+  }
+  detail::Session& s = sampler_session(t);
+  detail::check(sgdt_set_pool(s.get(), pool.data()), "sample_batch");
+  s.put_rng(rng);
+  out.resize(m);
+  detail::check(sgdt_sample_batch(s.get(), m, out.data()), "sample_batch");
+  s.take_rng(rng);
+  detail::check(sgdt_get_pool(s.get(), pool.data()), "sample_batch");
+}
+
+std::vector<std::uint32_t> sample_batch(const CooTensor& t, std::size_t m, Rng& rng) {
+  std::vector<std::uint32_t> pool, out;
+  sample_batch(t, m, rng, pool, out);
+  return out;
+}
+
+}  // namespace sptucker

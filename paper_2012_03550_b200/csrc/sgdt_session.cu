@@ -611,6 +611,27 @@ int sgdt_reset_pool(sgdt_session* s) {
   return SGDT_OK;
 }
 
+int sgdt_set_pool(sgdt_session* s, const uint32_t* pool) {
+  if (!s || !pool) return fail(SGDT_ERR_DOMAIN, "set_pool: null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  SGDT_CUDA(cudaMemcpyAsync(s->pool, pool, s->nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  s->pool_valid = true;
+  return SGDT_OK;
+}
+
+int sgdt_get_pool(sgdt_session* s, uint32_t* pool) {
+  if (!s || !pool) return fail(SGDT_ERR_DOMAIN, "get_pool: null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (!s->pool_valid) {
+    for (uint64_t e = 0; e < s->nnz; ++e) pool[e] = static_cast<uint32_t>(e);
+    return SGDT_OK;
+  }
+  SGDT_CUDA(cudaMemcpyAsync(pool, s->pool, s->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
 int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   if (m < 1 || m > s->nnz) return fail(SGDT_ERR_DOMAIN, "sample_batch: batch size out of range");
@@ -743,6 +764,20 @@ int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyp
 }
 
 uint64_t sgdt_launch_count(sgdt_session* s) { return s ? s->launches : 0; }
+
+uint64_t sgdt_workspace_bytes(sgdt_session* s) {
+  if (!s) return 0;
+  uint32_t js = 0;
+  for (int k = 0; k < s->order; ++k) js = std::max(js, s->J[k]);
+  uint64_t b = s->batch_cap * sizeof(uint32_t);
+  b += s->cs_cap * (static_cast<uint64_t>(js) + s->RP + 2) * sizeof(float);
+  b += 2ull * s->num_sms * js * sizeof(double);
+  if (s->batch_cap) b += 5ull * (s->batch_cap / (2 * s->order)) * sizeof(uint32_t);
+  uint32_t pieces = 0;
+  for (int n = 0; n < s->order; ++n) pieces = std::max(pieces, s->mode[n].n_pieces);
+  b += static_cast<uint64_t>(pieces) * s->RP * sizeof(double);
+  return b;
+}
 
 int sgdt_last_timing(sgdt_session* s, sgdt_timing* t) {
   if (!s || !t) return fail(SGDT_ERR_DOMAIN, "null argument");
