@@ -167,6 +167,49 @@ uint64_t sgdt_workspace_bytes(sgdt_session* s);
 /* Number of kernels this session has launched so far (all sgdt_* kernels). */
 uint64_t sgdt_launch_count(sgdt_session* s);
 
+/* ---- multi-GPU: sharded factor phase -------------
+ *
+ * A sharded session holds the full entry-order records (the replicated core
+ * phase draws and gathers the same Psi on every rank) but only this rank's
+ * slice partition_even(nnz, world)[rank] of every mode-sorted order -- the
+ * `improved` strategy's slices (factor_optimizer.cpp:209-210) with ranks in
+ * place of workers.  Per mode, a rank finalises the rows inside its slice and
+ * exports the <= 2 rows cut by the slice edges; the caller merges the exports
+ * of all ranks in rank order (factor_optimizer.cpp:247-270), finishes those
+ * rows, then publishes rows [row_lo, row_hi) of A^(n) to every rank and
+ * refreshes Q^(n).  paper_2012_03550_b200/distributed.py drives this over
+ * torch.distributed (NCCL on GPUs). */
+typedef struct {
+  int rank, world;
+  uint64_t entry_begin, entry_end; /* this rank's slice of the mode-sorted order */
+  uint32_t row_lo, row_hi;         /* rows this rank publishes after the mode */
+  uint32_t n_export;               /* rows cut by the slice edges (0..2) */
+  uint32_t export_rows[2];         /* 0-based row ids */
+} sgdt_shard_info;
+
+int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test,
+                              const uint32_t* J, uint32_t R, int device, int rank, int world,
+                              sgdt_session** out);
+int sgdt_get_shard_info(sgdt_session* s, int mode, sgdt_shard_info* out);
+/* Factor step of `mode` over this rank's slice; export_g receives n_export x R
+ * fp64 partial gradients g = sum (p - x) c of the cut rows. */
+int sgdt_factor_mode_local(sgdt_session* s, int mode, const sgdt_factor_hyper* h, double* export_g);
+/* Finalise k rows from merged gradients g (k x R fp64): F = B g, SGD step with
+ * the full bucket size as the batch count, Q row rewrite. */
+int sgdt_factor_mode_finish(sgdt_session* s, int mode, const sgdt_factor_hyper* h, uint32_t k,
+                            const uint32_t* rows, const double* g);
+/* Copy rows [row_lo, row_hi) of A^(mode) (fp32, J_mode per row) out of
+ * (to_device = 0) or into (1) the session; buf is host memory, or device
+ * memory when buf_on_device. */
+int sgdt_factor_rows(sgdt_session* s, int mode, uint32_t row_lo, uint32_t row_hi, float* buf,
+                     int to_device, int buf_on_device);
+/* Device address of A^(mode) (fp32, I_mode x J_mode row-major). */
+int sgdt_factor_device_ptr(sgdt_session* s, int mode, void** ptr);
+/* Q^(mode) = A^(mode) B^(mode) for every row. */
+int sgdt_refresh_q(sgdt_session* s, int mode);
+/* Wait for all work of the session (both of its streams). */
+int sgdt_synchronize(sgdt_session* s);
+
 /* Device next_below over an explicit MT state (test hook for the rejection
  * path, rng.hpp:20-25): draws n values with bounds[i] sequentially. */
 int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,

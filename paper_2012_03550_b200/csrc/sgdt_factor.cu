@@ -45,7 +45,8 @@ struct FactorArgs {
   uint32_t n_chunks;
   const SplitRow* splits;
   uint32_t n_splits;
-  double* piece;  // n_pieces x RP
+  double* piece;   // n_pieces x RP
+  double* xport;   // 2 x RP: summed pieces of rows cut by this rank's slice
   double lr, reg;
   int* flag;
 };
@@ -317,7 +318,29 @@ __global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
     for (int r = 0; r < RP; ++r) g[r] += src[r];
   }
   warp_allreduce<RP>(g);
-  if (lane == 0) finalize_row<RP>(a, bsn, sr.row, g);
+  if (lane != 0) return;
+  if (sr.pad) {  // cut by the slice edge: export for the rank-ordered merge
+    double* dst = a.xport + static_cast<uint64_t>(sr.pad - 1) * RP;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) dst[r] = g[r];
+  } else {
+    finalize_row<RP>(a, bsn, sr.row, g);
+  }
+}
+
+// Finalise rows whose gradient was merged across ranks (g: k x RP, fp64).
+template <int RP>
+__global__ void __launch_bounds__(256) factor_finish_kernel(FactorArgs a, uint32_t k, const uint32_t* rows,
+                                                            const double* gm) {
+  __shared__ float bsn[SGDT_MAX_J * RP];
+  load_bsn<RP>(a, bsn);
+  __syncthreads();
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  double g[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) g[r] = gm[static_cast<uint64_t>(t) * RP + r];
+  finalize_row<RP>(a, bsn, rows[t], g);
 }
 
 template <int RP, int NO>
@@ -338,6 +361,14 @@ int factor_launch(Session& s, FactorArgs& a) {
   return SGDT_OK;
 }
 
+template <int RP>
+int finish_launch(Session& s, FactorArgs& a, uint32_t k, const uint32_t* rows, const double* g) {
+  factor_finish_kernel<RP><<<(k + 255) / 256, 256, 0, s.stream>>>(a, k, rows, g);
+  SGDT_CUDA(cudaGetLastError());
+  ++s.launches;
+  return SGDT_OK;
+}
+
 template <int NO>
 int factor_launch_no(Session& s, FactorArgs& a) {
   switch (s.RP) {
@@ -354,9 +385,7 @@ int factor_launch_no(Session& s, FactorArgs& a) {
   return fail(SGDT_ERR_CONFIG, "unsupported R_core");
 }
 
-}  // namespace
-
-int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
+FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h) {
   const ModePlan& mp = s.mode[n];
   FactorArgs a{};
   a.P = s.P;
@@ -377,9 +406,17 @@ int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
   a.splits = mp.splits;
   a.n_splits = mp.n_splits;
   a.piece = s.piece_partials;
+  a.xport = s.export_buf;
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;
+  return a;
+}
+
+}  // namespace
+
+int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
+  FactorArgs a = factor_args(s, n, h);
   switch (s.order - 1) {
     case 1: return factor_launch_no<1>(s, a);
     case 2: return factor_launch_no<2>(s, a);
@@ -391,6 +428,24 @@ int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
     default: break;
   }
   return fail(SGDT_ERR_CONFIG, "unsupported tensor order");
+}
+
+int launch_factor_finish(Session& s, int n, const sgdt_factor_hyper& h, uint32_t k, const uint32_t* rows,
+                         const double* g) {
+  if (k == 0) return SGDT_OK;
+  FactorArgs a = factor_args(s, n, h);
+  switch (s.RP) {
+    case 4: return finish_launch<4>(s, a, k, rows, g);
+    case 8: return finish_launch<8>(s, a, k, rows, g);
+    case 12: return finish_launch<12>(s, a, k, rows, g);
+    case 16: return finish_launch<16>(s, a, k, rows, g);
+    case 20: return finish_launch<20>(s, a, k, rows, g);
+    case 24: return finish_launch<24>(s, a, k, rows, g);
+    case 28: return finish_launch<28>(s, a, k, rows, g);
+    case 32: return finish_launch<32>(s, a, k, rows, g);
+    default: break;
+  }
+  return fail(SGDT_ERR_CONFIG, "unsupported R_core");
 }
 
 }  // namespace sgdt

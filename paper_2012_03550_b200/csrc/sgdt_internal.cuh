@@ -35,11 +35,21 @@ struct Chunk {
 };
 
 // A row split over several chunks: pieces [first, first + count).
+// pad = 0: finalised on this device; pad = 1 + slot: the row is cut by this
+// rank's slice, its summed pieces go to export slot `slot` instead.
 struct SplitRow {
   uint32_t row;
   uint32_t first;
   uint32_t count;
   uint32_t pad;
+};
+
+// This rank's share of one mode (single GPU: the whole order).
+struct ShardPlan {
+  uint64_t qb = 0, qe = 0;        // slice [qb, qe) of the mode-sorted order
+  uint32_t row_lo = 0, row_hi = 0;  // rows this rank publishes after the mode
+  uint32_t n_export = 0;          // rows cut by the slice edges (<= 2)
+  uint32_t export_rows[2] = {0, 0};
 };
 
 struct RecordCopy {
@@ -58,6 +68,7 @@ struct ModePlan {
   uint32_t n_pieces = 0;
   uint64_t rows_nonempty = 0;
   uint64_t rows_empty = 0;
+  ShardPlan shard;
 };
 
 struct Params {
@@ -78,6 +89,7 @@ struct Session {
   cudaStream_t side = nullptr;  // sampler run-ahead (Psi does not depend on the model)
   cudaEvent_t ev_start = nullptr, ev_core = nullptr, ev_samp = nullptr;
   int order = 0;
+  int rank = 0, world = 1;  // sharded factor phase (multi-GPU)
   uint32_t dims[kMaxOrder] = {};
   uint32_t J[kMaxOrder] = {};
   uint32_t R = 0, RP = 0;
@@ -89,6 +101,7 @@ struct Session {
 
   Params P{};
   double* piece_partials = nullptr;  // max pieces x RP
+  double* export_buf = nullptr;      // 2 x RP, boundary-row partials of the last mode run
 
   // sampler state
   uint64_t* mt = nullptr;       // 312 words + position word
@@ -152,6 +165,8 @@ int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, u
                 int per_mode_batches);
 int launch_q_refresh(Session& s, int mode);
 int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h);
+int launch_factor_finish(Session& s, int n, const sgdt_factor_hyper& h, uint32_t k, const uint32_t* rows_dev,
+                         const double* g_dev);
 int launch_eval(Session& s, int which, double* rmse, double* mae);
 int launch_cast_model(Session& s, int to_device, int n, double* stage);
 

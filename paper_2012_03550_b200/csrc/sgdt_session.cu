@@ -39,15 +39,16 @@ __global__ void build_entry_copy_kernel(const uint32_t* __restrict__ coords,
 }
 
 // Mode-sorted copy: record q of mode n is entry perm[q] (sptensor.cpp:102-117).
+// len records of the slice: record q is entry perm[q] (src copy has nnz records).
 __global__ void gather_mode_copy_kernel(const uint32_t* __restrict__ src_idx,
                                         const float* __restrict__ src_val,
-                                        const uint32_t* __restrict__ perm, uint64_t nnz, int order,
-                                        uint32_t* idx, float* val) {
-  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nnz;
+                                        const uint32_t* __restrict__ perm, uint64_t nnz, uint64_t len,
+                                        int order, uint32_t* idx, float* val) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < len;
        q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t e = perm[q];
     for (int k = 0; k < order; ++k)
-      idx[static_cast<uint64_t>(k) * nnz + q] = src_idx[static_cast<uint64_t>(k) * nnz + e];
+      idx[static_cast<uint64_t>(k) * len + q] = src_idx[static_cast<uint64_t>(k) * nnz + e];
     val[q] = src_val[e];
   }
 }
@@ -133,40 +134,56 @@ void host_mode_layout(const sgdt_tensor_desc* d, int n, std::vector<uint64_t>& o
   for (uint64_t e = 0; e < d->nnz; ++e) perm[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
 }
 
-// nnz-balanced chunk schedule over the mode-sorted entries: whole rows packed
-// greedily up to chunk_size, longer rows cut into pieces of chunk_size.
-void build_chunks(const std::vector<uint64_t>& off, uint32_t chunk_size, std::vector<Chunk>& chunks,
-                  std::vector<SplitRow>& splits, uint32_t& n_pieces, uint64_t& nonempty) {
+// nnz-balanced chunk schedule over the mode-sorted entries [qb, qe) (the
+// whole order for a single-GPU session; this rank's partition_even slice for a
+// sharded one): whole rows packed greedily up to chunk_size, longer rows cut
+// into pieces of chunk_size.  A row cut by the slice edges is not finalised
+// here: its pieces are summed into an export slot for the cross-rank merge
+// (the rank-ordered boundary merge of factor_optimizer.cpp:247-270).  Chunk
+// bounds are relative to qb.
+void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, uint32_t chunk_size,
+                  std::vector<Chunk>& chunks, std::vector<SplitRow>& splits, uint32_t& n_pieces, ShardPlan& sp) {
   chunks.clear();
   splits.clear();
   n_pieces = 0;
-  nonempty = 0;
+  sp = ShardPlan{};
+  sp.qb = qb;
+  sp.qe = qe;
+  if (qb >= qe) return;
   const size_t rows = off.size() - 1;
+  // row holding position q: off[i] <= q < off[i+1]
+  auto row_of = [&](uint64_t q) {
+    return static_cast<size_t>(std::upper_bound(off.begin(), off.end(), q) - off.begin()) - 1;
+  };
+  const size_t r0 = row_of(qb), r1 = row_of(qe - 1);
+  sp.row_lo = static_cast<uint32_t>(off[r0] < qb ? r0 + 1 : r0);
+  sp.row_hi = static_cast<uint32_t>(r1 + 1);
   bool open = false;
   Chunk cur{0, 0, -1, 0};
-  for (size_t i = 0; i < rows; ++i) {
-    const uint64_t b = off[i], e = off[i + 1], cnt = e - b;
-    if (cnt == 0) continue;
-    ++nonempty;
-    if (cnt > chunk_size) {
-      if (open) {
-        chunks.push_back(cur);
-        open = false;
-      }
+  auto close = [&] {
+    if (open) chunks.push_back(cur);
+    open = false;
+  };
+  for (size_t i = r0; i <= r1 && i < rows; ++i) {
+    if (off[i + 1] == off[i]) continue;
+    const uint64_t b = std::max(off[i], qb) - qb, e = std::min(off[i + 1], qe) - qb, cnt = e - b;
+    const bool cut = off[i] < qb || off[i + 1] > qe;
+    if (cut || cnt > chunk_size) {
+      close();
       SplitRow sr{static_cast<uint32_t>(i), n_pieces, 0, 0};
+      if (cut) {
+        sr.pad = 1 + sp.n_export;
+        sp.export_rows[sp.n_export++] = static_cast<uint32_t>(i);
+      }
       for (uint64_t p = b; p < e; p += chunk_size) {
         const uint64_t pe = std::min<uint64_t>(p + chunk_size, e);
-        chunks.push_back(Chunk{static_cast<uint32_t>(p), static_cast<uint32_t>(pe),
-                               static_cast<int32_t>(n_pieces++), 0});
+        chunks.push_back(Chunk{static_cast<uint32_t>(p), static_cast<uint32_t>(pe), static_cast<int32_t>(n_pieces++), 0});
         ++sr.count;
       }
       splits.push_back(sr);
       continue;
     }
-    if (open && (e - cur.begin) > chunk_size) {
-      chunks.push_back(cur);
-      open = false;
-    }
+    if (open && (e - cur.begin) > chunk_size) close();
     if (!open) {
       cur = Chunk{static_cast<uint32_t>(b), static_cast<uint32_t>(e), -1, 0};
       open = true;
@@ -174,7 +191,7 @@ void build_chunks(const std::vector<uint64_t>& off, uint32_t chunk_size, std::ve
       cur.end = static_cast<uint32_t>(e);
     }
   }
-  if (open) chunks.push_back(cur);
+  close();
 }
 
 int upload_record_copy(Session& s, const sgdt_tensor_desc* d, RecordCopy& rc, uint32_t** d_coords_keep,
@@ -230,6 +247,7 @@ void free_session(sgdt_session* s) {
     F(s->P.Q[n]);
   }
   F(s->piece_partials);
+  F(s->export_buf);
   F(s->mt);
   F(s->pool);
   F(s->head);
@@ -409,7 +427,13 @@ void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uin
 
 int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test, const uint32_t* J,
                         uint32_t R, int device, sgdt_session** out) {
+  return sgdt_session_create_shard(train, test, J, R, device, 0, 1, out);
+}
+
+int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test, const uint32_t* J,
+                              uint32_t R, int device, int rank, int world, sgdt_session** out) {
   if (!out) return fail(SGDT_ERR_DOMAIN, "out is null");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SGDT_ERR_DOMAIN, "shard: need 0 <= rank < world");
   *out = nullptr;
   TRY(validate_desc(train, "train"));
   if (test) {
@@ -445,6 +469,8 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
     }
     s->order = train->order;
     s->nnz = train->nnz;
+    s->rank = rank;
+    s->world = world;
     s->R = R;
     s->RP = (R + 3) & ~3u;
     s->P.order = s->order;
@@ -465,13 +491,24 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
       ModePlan& mp = s->mode[n];
       host_mode_layout(train, n, off, perm);
       const uint32_t* hperm = (train->mode_perm && train->mode_perm[n]) ? train->mode_perm[n] : perm.data();
-      SGDT_CUDA(cudaMemcpyAsync(d_perm, hperm, s->nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
-      mp.rec.nnz = s->nnz;
-      TRY(dalloc(&mp.rec.idx, s->nnz * s->order));
-      TRY(dalloc(&mp.rec.val, s->nnz));
-      gather_mode_copy_kernel<<<grid_for(s->nnz, s->num_sms), 256, 0, s->stream>>>(
-          s->train_rec.idx, s->train_rec.val, d_perm, s->nnz, s->order, mp.rec.idx, mp.rec.val);
-      SGDT_CUDA(cudaGetLastError());
+      // this rank's slice of the mode-n order (partition_even, scheduler.cpp:34-46)
+      uint64_t qb = 0, qe = 0;
+      {
+        std::vector<uint64_t> pb(world), pe(world);
+        sgdt_partition_even(s->nnz, static_cast<uint64_t>(world), pb.data(), pe.data());
+        qb = pb[rank];
+        qe = pe[rank];
+      }
+      const uint64_t len = qe - qb;
+      if (len) SGDT_CUDA(cudaMemcpyAsync(d_perm, hperm + qb, len * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+      mp.rec.nnz = len;
+      TRY(dalloc(&mp.rec.idx, len * s->order));
+      TRY(dalloc(&mp.rec.val, len));
+      if (len) {
+        gather_mode_copy_kernel<<<grid_for(len, s->num_sms), 256, 0, s->stream>>>(
+            s->train_rec.idx, s->train_rec.val, d_perm, s->nnz, len, s->order, mp.rec.idx, mp.rec.val);
+        SGDT_CUDA(cudaGetLastError());
+      }
       std::vector<uint32_t> rp(off.size());
       for (size_t i = 0; i < off.size(); ++i) rp[i] = static_cast<uint32_t>(off[i]);
       TRY(dalloc(&mp.row_ptr, rp.size()));
@@ -479,7 +516,9 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
                                 s->stream));
       std::vector<Chunk> chunks;
       std::vector<SplitRow> splits;
-      build_chunks(off, s->chunk_size, chunks, splits, mp.n_pieces, mp.rows_nonempty);
+      build_chunks(off, qb, qe, s->chunk_size, chunks, splits, mp.n_pieces, mp.shard);
+      mp.rows_nonempty = 0;
+      for (size_t i = 0; i + 1 < off.size(); ++i) mp.rows_nonempty += off[i + 1] > off[i];
       mp.rows_empty = s->dims[n] - mp.rows_nonempty;
       mp.n_chunks = static_cast<uint32_t>(chunks.size());
       mp.n_splits = static_cast<uint32_t>(splits.size());
@@ -514,6 +553,7 @@ int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* t
     TRY(dalloc(&s->stage, stage));
     s->stage_cap = stage;
     TRY(dalloc(&s->piece_partials, static_cast<uint64_t>(std::max<uint32_t>(max_pieces, 1)) * s->RP));
+    TRY(dalloc(&s->export_buf, 2ull * s->RP));
     // sampler
     TRY(dalloc(&s->mt, 313));
     uint64_t mt[313];
@@ -764,6 +804,109 @@ int sgdt_train(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyp
 }
 
 uint64_t sgdt_launch_count(sgdt_session* s) { return s ? s->launches : 0; }
+
+int sgdt_get_shard_info(sgdt_session* s, int mode, sgdt_shard_info* out) {
+  if (!s || !out) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "shard_info: mode out of range");
+  const ShardPlan& sp = s->mode[mode].shard;
+  out->rank = s->rank;
+  out->world = s->world;
+  out->entry_begin = sp.qb;
+  out->entry_end = sp.qe;
+  out->row_lo = sp.row_lo;
+  out->row_hi = sp.row_hi;
+  out->n_export = sp.n_export;
+  out->export_rows[0] = sp.export_rows[0];
+  out->export_rows[1] = sp.export_rows[1];
+  return SGDT_OK;
+}
+
+int sgdt_factor_mode_local(sgdt_session* s, int mode, const sgdt_factor_hyper* h, double* export_g) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_mode_local: mode out of range");
+  TRY(check_factor_hyper(h));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (h->lr == 0.0) return SGDT_OK;
+  TRY(launch_factor_mode(*s, mode, *h));
+  const ShardPlan& sp = s->mode[mode].shard;
+  std::vector<double> buf(2ull * s->RP);
+  if (sp.n_export)
+    SGDT_CUDA(cudaMemcpyAsync(buf.data(), s->export_buf, sp.n_export * s->RP * sizeof(double),
+                              cudaMemcpyDeviceToHost, s->stream));
+  TRY(sync_and_flag(*s));
+  if (export_g)
+    for (uint32_t k = 0; k < sp.n_export; ++k)
+      for (uint32_t r = 0; r < s->R; ++r) export_g[k * s->R + r] = buf[k * s->RP + r];
+  return SGDT_OK;
+}
+
+int sgdt_factor_mode_finish(sgdt_session* s, int mode, const sgdt_factor_hyper* h, uint32_t k, const uint32_t* rows,
+                            const double* g) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_mode_finish: mode out of range");
+  TRY(check_factor_hyper(h));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (h->lr == 0.0 || k == 0) return SGDT_OK;
+  for (uint32_t i = 0; i < k; ++i)
+    if (rows[i] >= s->dims[mode]) return fail(SGDT_ERR_DOMAIN, "factor_mode_finish: row out of range");
+  std::vector<double> gp(static_cast<uint64_t>(k) * s->RP, 0.0);
+  for (uint32_t i = 0; i < k; ++i)
+    for (uint32_t r = 0; r < s->R; ++r) gp[i * s->RP + r] = g[i * s->R + r];
+  uint32_t* d_rows = nullptr;
+  double* d_g = nullptr;
+  TRY(dalloc(&d_rows, k));
+  TRY(dalloc(&d_g, gp.size()));
+  SGDT_CUDA(cudaMemcpyAsync(d_rows, rows, k * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+  SGDT_CUDA(cudaMemcpyAsync(d_g, gp.data(), gp.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  const int rc = launch_factor_finish(*s, mode, *h, k, d_rows, d_g);
+  const int rc2 = sync_and_flag(*s);
+  cudaFree(d_rows);
+  cudaFree(d_g);
+  return rc ? rc : rc2;
+}
+
+int sgdt_factor_rows(sgdt_session* s, int mode, uint32_t row_lo, uint32_t row_hi, float* buf, int to_device,
+                     int buf_on_device) {
+  if (!s || (!buf && row_hi > row_lo)) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (mode < 0 || mode >= s->order || row_lo > row_hi || row_hi > s->dims[mode])
+    return fail(SGDT_ERR_DOMAIN, "factor_rows: range out of bounds");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (row_hi == row_lo) return SGDT_OK;
+  float* dev = s->P.A[mode] + static_cast<uint64_t>(row_lo) * s->J[mode];
+  const size_t bytes = static_cast<size_t>(row_hi - row_lo) * s->J[mode] * sizeof(float);
+  const cudaMemcpyKind kind = buf_on_device ? cudaMemcpyDeviceToDevice
+                                            : (to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost);
+  if (to_device)
+    SGDT_CUDA(cudaMemcpyAsync(dev, buf, bytes, kind, s->stream));
+  else
+    SGDT_CUDA(cudaMemcpyAsync(buf, dev, bytes, kind, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_factor_device_ptr(sgdt_session* s, int mode, void** ptr) {
+  if (!s || !ptr) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_device_ptr: mode out of range");
+  *ptr = s->P.A[mode];
+  return SGDT_OK;
+}
+
+int sgdt_refresh_q(sgdt_session* s, int mode) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "refresh_q: mode out of range");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(launch_q_refresh(*s, mode));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  return SGDT_OK;
+}
+
+int sgdt_synchronize(sgdt_session* s) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->side));
+  return SGDT_OK;
+}
 
 uint64_t sgdt_workspace_bytes(sgdt_session* s) {
   if (!s) return 0;

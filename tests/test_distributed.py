@@ -1,0 +1,149 @@
+"""Multi-rank factor phase (paper_2012_03550_b200/distributed.py).
+
+CPU: the orchestration (partition_even slices, boundary export, rank-ordered
+merge, row publication) on a numpy stand-in session, with in-process thread
+ranks and with 2 torch.distributed gloo processes; results must equal the
+single-rank run and the oracle's serial factor epoch.
+GPU: real sharded sessions (2 and 3 ranks as threads on one GPU) against the
+single-session device result and the oracle."""
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import oracle_py as O
+from paper_2012_03550_b200 import distributed as D
+
+from cpu_shard_backend import CpuShard
+
+DIMS, J, R = (7, 40, 30), (3, 3, 3), 3
+
+
+class FH:  # FactorHyper look-alike for the CPU backend
+    lr, reg, row_fraction = 0.02, 0.01, 1.0
+
+
+def data(nnz=2500, seed=5):
+    c, v = O.synth_planted(DIMS, J, R, nnz, 0.05, 0.0, 0.6, seed)
+    m = O.Model(DIMS, J, R).init_gaussian(0.0, 0.6, seed + 1)
+    return c, v, m.params()
+
+
+def oracle_factor(c, v, A, B):
+    m = O.Model(DIMS, J, R)
+    m.set_params(A, B)
+    O.update_factor_epoch(m, O.Tensor(DIMS, c, v), FH.lr, FH.reg, O.Rng(1))
+    return m.params()[0]
+
+
+def run_threads(c, v, A, B, world):
+    groups = D.ThreadGroup.make(world)
+    sess = [CpuShard(DIMS, c, v, J, R, r, world, A, B) for r in range(world)]
+    errs = []
+
+    def body(r):
+        try:
+            D.factor_epoch_sharded(sess[r], groups[r], FH)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            raise
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    return sess
+
+
+def test_merge_boundary_is_rank_ordered_sum():
+    recs = [D.pack_boundary([5], np.array([[1.0, 2.0]]), 2),
+            D.pack_boundary([5, 9], np.array([[10.0, 20.0], [1.0, 1.0]]), 2),
+            D.pack_boundary([], np.zeros((0, 2)), 2),
+            D.pack_boundary([9], np.array([[0.5, 0.5]]), 2)]
+    m = D.merge_boundary(recs, 2)
+    assert sorted(m) == [5, 9]
+    assert np.array_equal(m[5], [11.0, 22.0]) and np.array_equal(m[9], [1.5, 1.5])
+
+
+@pytest.mark.parametrize("world", [2, 3, 7, 16])
+def test_thread_ranks_match_single_rank_and_oracle(world):
+    c, v, (A, B) = data()
+    one = run_threads(c, v, A, B, 1)[0]
+    ref = oracle_factor(c, v, A, B)
+    for n in range(3):
+        assert np.max(np.abs(one.A[n] - ref[n])) <= 1e-9
+    ranks = run_threads(c, v, A, B, world)
+    for s in ranks:  # every rank holds the full, identical result
+        for n in range(3):
+            assert np.max(np.abs(s.A[n] - one.A[n])) <= 1e-12
+
+
+def _gloo_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c, v, (A, B) = data()
+    s = CpuShard(DIMS, c, v, J, R, rank, world, A, B)
+    D.factor_epoch_sharded(s, D.TorchGroup(), FH)
+    np.save(os.path.join(out_dir, f"A_{rank}.npy"), np.concatenate([a.ravel() for a in s.A]))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_processes(tmp_path):
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.spawn(_gloo_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    c, v, (A, B) = data()
+    one = run_threads(c, v, A, B, 1)[0]
+    want = np.concatenate([a.ravel() for a in one.A])
+    for r in range(2):
+        got = np.load(tmp_path / f"A_{r}.npy")
+        assert np.max(np.abs(got - want)) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_sharded_sessions_match_single_session(world):
+    from paper_2012_03550_b200 import sgdt
+    c, v, (A, B) = data(nnz=6000, seed=9)
+    A = [a.astype(np.float32).astype(np.float64) for a in A]
+    B = [b.astype(np.float32).astype(np.float64) for b in B]
+    fh = sgdt.FactorHyper(FH.lr, FH.reg, 1.0)
+    ch = sgdt.CoreHyper(0.01, 0.01, 256, 0, 0)
+    single = sgdt.Session(DIMS, c, v, J, R)
+    single.set_model(A, B)
+    single.seed(4)
+    single.core_epoch(ch.lr, ch.reg, ch.batch_m)
+    single.factor_epoch(fh.lr, fh.reg)
+    SA, SB = single.get_model()
+    groups = D.ThreadGroup.make(world)
+    sess = [D.ShardedSession(DIMS, c, v, J, R, r, world) for r in range(world)]
+    for s in sess:
+        s.set_model(A, B)
+        s.seed(4)
+    errs = []
+
+    def body(r):
+        try:
+            D.run_epochs_sharded(sess[r], groups[r], ch, fh, 1)
+        except Exception as e:
+            errs.append(e)
+            raise
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for s in sess:
+        GA, GB = s.get_model()
+        for n in range(3):
+            assert np.array_equal(GB[n], SB[n])  # replicated core phase: bit-identical
+            assert np.max(np.abs(GA[n] - SA[n]) / np.maximum(1, np.abs(SA[n]))) <= 1e-5
