@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_NNZ)
+    p.add_argument("--sharded", action="store_true",
+                   help="use the multi-GPU (sharded factor phase) driver even on one rank")
     return p.parse_args()
 
 
@@ -289,7 +291,7 @@ def run_sharded(args, rank, world, local_rank):
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2012_03550_b200 import sgdt
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_sharded(args, rank, world, local_rank)
     torch.cuda.set_device(local_rank)
     dist = None

@@ -147,3 +147,40 @@ def test_gpu_sharded_sessions_match_single_session(world):
         for n in range(3):
             assert np.array_equal(GB[n], SB[n])  # replicated core phase: bit-identical
             assert np.max(np.abs(GA[n] - SA[n]) / np.maximum(1, np.abs(SA[n]))) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_gpu_nccl_path_single_rank():
+    """The NCCL publication path (torch tensor aliasing the session's A^(n),
+    dist.broadcast on it) at world size 1."""
+    import torch
+    import torch.distributed as dist
+    from paper_2012_03550_b200 import sgdt
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        c, v, (A, B) = data(nnz=6000, seed=9)
+        fh = sgdt.FactorHyper(FH.lr, FH.reg, 1.0)
+        ch = sgdt.CoreHyper(0.01, 0.01, 256, 0, 0)
+        single = sgdt.Session(DIMS, c, v, J, R)
+        single.set_model(A, B)
+        single.seed(4)
+        single.run_epochs(ch, fh, 2)
+        s = D.ShardedSession(DIMS, c, v, J, R, 0, 1)
+        s.set_model(A, B)
+        s.seed(4)
+        g = D.TorchGroup()
+        assert g.nccl
+        D.run_epochs_sharded(s, g, ch, fh, 2)
+        a = s.factor_tensor(0)
+        assert a.is_cuda and tuple(a.shape) == (DIMS[0], J[0])
+        SA, SB = single.get_model()
+        GA, GB = s.get_model()
+        for n in range(3):
+            assert np.array_equal(GA[n], SA[n]) and np.array_equal(GB[n], SB[n])
+    finally:
+        dist.destroy_process_group()
