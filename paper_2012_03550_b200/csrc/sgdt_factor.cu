@@ -385,26 +385,28 @@ int factor_launch_no(Session& s, FactorArgs& a) {
   return fail(SGDT_ERR_CONFIG, "unsupported R_core");
 }
 
-FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h) {
+FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h, bool subset = false) {
   const ModePlan& mp = s.mode[n];
+  const RowSubset& rs = mp.subset;
+  const RecordCopy& rec = subset ? rs.rec : mp.rec;
   FactorArgs a{};
   a.P = s.P;
   a.n = n;
-  a.keys = mp.rec.idx + static_cast<uint64_t>(n) * mp.rec.nnz;
-  a.val = mp.rec.val;
+  a.keys = rec.idx + static_cast<uint64_t>(n) * rec.nnz;
+  a.val = rec.val;
   int j = 0;
   for (int k = 0; k < s.order; ++k) {
     if (k == n) continue;
-    a.oidx[j] = mp.rec.idx + static_cast<uint64_t>(k) * mp.rec.nnz;
+    a.oidx[j] = rec.idx + static_cast<uint64_t>(k) * rec.nnz;
     a.oq[j] = s.P.Q[k];
     ++j;
   }
-  a.nnz = mp.rec.nnz;
-  a.row_ptr = mp.row_ptr;
-  a.chunks = mp.chunks;
-  a.n_chunks = mp.n_chunks;
-  a.splits = mp.splits;
-  a.n_splits = mp.n_splits;
+  a.nnz = rec.nnz;
+  a.row_ptr = subset ? rs.sub_off : mp.row_ptr;  // the batch count of a row is its kept subset
+  a.chunks = subset ? rs.chunks : mp.chunks;
+  a.n_chunks = subset ? rs.n_chunks : mp.n_chunks;
+  a.splits = subset ? rs.splits : mp.splits;
+  a.n_splits = subset ? rs.n_splits : mp.n_splits;
   a.piece = s.piece_partials;
   a.xport = s.export_buf;
   a.lr = h.lr;
@@ -415,8 +417,8 @@ FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h) {
 
 }  // namespace
 
-int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h) {
-  FactorArgs a = factor_args(s, n, h);
+int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h, bool subset) {
+  FactorArgs a = factor_args(s, n, h, subset);
   switch (s.order - 1) {
     case 1: return factor_launch_no<1>(s, a);
     case 2: return factor_launch_no<2>(s, a);

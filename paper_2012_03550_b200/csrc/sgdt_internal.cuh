@@ -58,6 +58,22 @@ struct RecordCopy {
   uint64_t nnz = 0;
 };
 
+// row_fraction < 1: the per-epoch row subsets of one mode (draw scratch,
+// subset records and their chunk schedule; rebuilt when the fraction changes).
+struct RowSubset {
+  double fraction = -1.0;
+  uint64_t total = 0;           // draws = kept entries, sum_i keep_i
+  uint32_t* sub_off = nullptr;  // I_n + 1 prefix sums of keep (the subset's row_ptr)
+  uint32_t *target = nullptr, *pos = nullptr, *link = nullptr, *kprev = nullptr, *lprev = nullptr,
+           *out = nullptr;      // per draw
+  RecordCopy rec;               // kept records, row-grouped
+  struct Chunk* chunks = nullptr;
+  uint32_t n_chunks = 0;
+  struct SplitRow* splits = nullptr;
+  uint32_t n_splits = 0;
+  uint32_t n_pieces = 0;
+};
+
 struct ModePlan {
   RecordCopy rec;
   uint32_t* row_ptr = nullptr;  // I_n + 1
@@ -69,6 +85,7 @@ struct ModePlan {
   uint64_t rows_nonempty = 0;
   uint64_t rows_empty = 0;
   ShardPlan shard;
+  RowSubset subset;
 };
 
 struct Params {
@@ -98,6 +115,8 @@ struct Session {
 
   RecordCopy train_rec, test_rec;
   ModePlan mode[kMaxOrder];
+  std::vector<uint64_t> h_row_ptr[kMaxOrder];  // host copy of every mode's bucket offsets
+  uint32_t piece_cap = 0;                       // rows of piece_partials
 
   Params P{};
   double* piece_partials = nullptr;  // max pieces x RP
@@ -164,7 +183,8 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st)
 int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, uint64_t m,
                 int per_mode_batches);
 int launch_q_refresh(Session& s, int mode);
-int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h);
+int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h, bool subset = false);
+int launch_row_subsets(Session& s, int n, RowSubset& rs, cudaStream_t st);
 int launch_factor_finish(Session& s, int n, const sgdt_factor_hyper& h, uint32_t k, const uint32_t* rows_dev,
                          const double* g_dev);
 int launch_eval(Session& s, int which, double* rmse, double* mae);

@@ -60,13 +60,58 @@ __device__ void mt_twist(uint64_t* x) {
   __syncthreads();
 }
 
-// Draw `m` values sequentially.  MODE 0: sampler draws, bound = nnz - d,
-// result j_d = d + r % bound stored as u32.  MODE 1: explicit u64 bounds,
-// result r % bound stored as u64 (test hook).
-template <int MODE>
-__global__ void __launch_bounds__(320) mt_draw_kernel(uint64_t* state, uint64_t m, uint64_t nnz,
-                                                      const uint64_t* bounds, uint32_t* out32,
-                                                      uint64_t* out64) {
+// What a run of sequential next_below draws means.
+//   BATCH:  draw d of sample_batch: bound = nnz - d, target = d + r % bound
+//           (sptensor.cpp:265-268), position d.
+//   BOUNDS: explicit u64 bounds (test hook), raw value r % bound.
+//   ROWS:   row_fraction < 1 (factor_optimizer.cpp:143-165): draws are grouped
+//           by row (rows ascending, sub_off = prefix sums of keep); draw q of
+//           row i has bound bs_i - q, position row_ptr[i] + q and target
+//           position + r % bound inside the bucket.
+struct DrawPlan {
+  int kind;  // 0 BATCH, 1 BOUNDS, 2 ROWS
+  uint64_t nnz;
+  const uint64_t* bounds;
+  const uint32_t* sub_off;
+  uint32_t n_rows;
+  const uint32_t* row_ptr;
+  uint32_t* out_target;
+  uint32_t* out_pos;
+  uint64_t* out64;
+};
+
+__device__ __forceinline__ uint64_t plan_bound(const DrawPlan& p, uint64_t d, uint64_t* base) {
+  if (p.kind == 0) {
+    *base = d;
+    return p.nnz - d;
+  }
+  if (p.kind == 1) {
+    *base = 0;
+    return p.bounds[d];
+  }
+  uint32_t lo = 0, hi = p.n_rows;  // largest row with sub_off[row] <= d
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p.sub_off[mid] <= d) lo = mid; else hi = mid;
+  }
+  const uint64_t q = d - p.sub_off[lo];
+  *base = p.row_ptr[lo] + q;
+  return static_cast<uint64_t>(p.row_ptr[lo + 1] - p.row_ptr[lo]) - q;
+}
+
+__device__ __forceinline__ void plan_store(const DrawPlan& p, uint64_t d, uint64_t base, uint64_t v) {
+  if (p.kind == 1) {
+    p.out64[d] = v;
+    return;
+  }
+  p.out_target[d] = static_cast<uint32_t>(base + v);
+  if (p.out_pos) p.out_pos[d] = static_cast<uint32_t>(base);
+}
+
+// m draws in stream order.  Each block of 312 tempered outputs is mapped
+// optimistically to consecutive draws; a block containing a rejection is
+// replayed by lane 0 so exactly the reference's outputs are consumed.
+__global__ void __launch_bounds__(320) mt_draw_kernel(uint64_t* state, uint64_t m, DrawPlan plan) {
   __shared__ uint64_t x[kMtN];
   __shared__ uint64_t s_done, s_pos;
   const int t = threadIdx.x;
@@ -86,40 +131,29 @@ __global__ void __launch_bounds__(320) mt_draw_kernel(uint64_t* state, uint64_t 
     }
     const uint64_t avail = kMtN - pos;
     const uint64_t take = (m - done) < avail ? (m - done) : avail;
-    uint64_t r = 0, bound = 1, d = done + t;
+    uint64_t r = 0, bound = 1, base = 0, d = done + t;
     int rej = 0;
     if (t < take) {
       r = temper(x[pos + t]);
-      bound = MODE == 0 ? nnz - d : bounds[d];
-      const uint64_t thr = (0ULL - bound) % bound;
-      rej = r < thr;
+      bound = plan_bound(plan, d, &base);
+      rej = r < (0ULL - bound) % bound;
     }
     const int any = __syncthreads_or(rej);
     if (!any) {
-      if (t < take) {
-        const uint64_t v = r % bound;
-        if (MODE == 0)
-          out32[d] = static_cast<uint32_t>(d + v);
-        else
-          out64[d] = v;
-      }
+      if (t < take) plan_store(plan, d, base, r % bound);
       __syncthreads();
       if (t == 0) {
         s_done = done + take;
         s_pos = pos + take;
       }
     } else if (t == 0) {
-      // Rare path: replay this block sequentially, consuming outputs exactly.
       uint64_t dd = done, p = pos;
       while (dd < m && p < kMtN) {
         const uint64_t rr = temper(x[p++]);
-        const uint64_t b = MODE == 0 ? nnz - dd : bounds[dd];
-        const uint64_t thr = (0ULL - b) % b;
-        if (rr < thr) continue;
-        if (MODE == 0)
-          out32[dd] = static_cast<uint32_t>(dd + rr % b);
-        else
-          out64[dd] = rr % b;
+        uint64_t bb = 0;
+        const uint64_t b = plan_bound(plan, dd, &bb);
+        if (rr < (0ULL - b) % b) continue;
+        plan_store(plan, dd, bb, rr % b);
         ++dd;
       }
       s_done = dd;
@@ -158,29 +192,34 @@ __device__ __forceinline__ uint32_t list_max_below(const unsigned long long* hea
   return best;
 }
 
-__global__ void resolve_kernel(uint64_t m, const uint32_t* __restrict__ jd,
+// pos: position of each draw (nullptr: draw i sits at position i).
+__global__ void resolve_kernel(uint64_t m, const uint32_t* __restrict__ jd, const uint32_t* __restrict__ pos,
                                const unsigned long long* head, const uint32_t* link,
                                uint32_t stamp, uint32_t* kprev, uint32_t* lprev) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= m) return;
+  const uint32_t p = pos ? pos[i] : static_cast<uint32_t>(i);
   kprev[i] = list_max_below(head, link, stamp, jd[i], static_cast<uint32_t>(i));
-  lprev[i] = list_max_below(head, link, stamp, static_cast<uint32_t>(i), static_cast<uint32_t>(i));
+  lprev[i] = list_max_below(head, link, stamp, p, static_cast<uint32_t>(i));
 }
 
-__device__ __forceinline__ uint32_t chain_value(const uint32_t* pool, const uint32_t* lprev,
-                                                uint32_t x) {
+// D(x): value at draw x's position just before step x.  pool == nullptr:
+// the initial pool is the identity (row subsets start from bucket order).
+__device__ __forceinline__ uint32_t chain_value(const uint32_t* pool, const uint32_t* pos,
+                                                const uint32_t* lprev, uint32_t x) {
   while (lprev[x] != kNone) x = lprev[x];
-  return pool[x];
+  const uint32_t p = pos ? pos[x] : x;
+  return pool ? pool[p] : p;
 }
 
-__global__ void chain_kernel(uint64_t m, const uint32_t* __restrict__ pool,
+__global__ void chain_kernel(uint64_t m, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ pos,
                              const uint32_t* __restrict__ jd, const uint32_t* kprev,
                              const uint32_t* lprev, uint32_t* dval, uint32_t* out) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= m) return;
-  dval[i] = chain_value(pool, lprev, static_cast<uint32_t>(i));
+  if (dval) dval[i] = chain_value(pool, pos, lprev, static_cast<uint32_t>(i));
   const uint32_t k = kprev[i];
-  out[i] = k == kNone ? pool[jd[i]] : chain_value(pool, lprev, k);
+  out[i] = k == kNone ? (pool ? pool[jd[i]] : jd[i]) : chain_value(pool, pos, lprev, k);
 }
 
 __global__ void write_pool_kernel(uint64_t m, uint32_t* pool, const uint32_t* __restrict__ jd,
@@ -209,18 +248,51 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st)
     SGDT_CUDA(cudaMemsetAsync(s.head, 0, s.nnz * sizeof(unsigned long long), st));
     s.stamp = 1;
   }
-  mt_draw_kernel<0><<<1, 320, 0, st>>>(s.mt, m, s.nnz, nullptr, s.draw_j, nullptr);
+  DrawPlan plan{};
+  plan.kind = 0;
+  plan.nnz = s.nnz;
+  plan.out_target = s.draw_j;
+  mt_draw_kernel<<<1, 320, 0, st>>>(s.mt, m, plan);
   SGDT_CUDA(cudaGetLastError());
   const unsigned blocks = static_cast<unsigned>((m + 255) / 256);
   link_kernel<<<blocks, 256, 0, st>>>(m, s.draw_j, s.head, s.stamp, s.link);
-  resolve_kernel<<<blocks, 256, 0, st>>>(m, s.draw_j, s.head, s.link, s.stamp, s.kprev, s.lprev);
-  chain_kernel<<<blocks, 256, 0, st>>>(m, s.pool, s.draw_j, s.kprev, s.lprev, s.dval, out_batch);
+  resolve_kernel<<<blocks, 256, 0, st>>>(m, s.draw_j, nullptr, s.head, s.link, s.stamp, s.kprev, s.lprev);
+  chain_kernel<<<blocks, 256, 0, st>>>(m, s.pool, nullptr, s.draw_j, s.kprev, s.lprev, s.dval, out_batch);
   write_pool_kernel<<<blocks, 256, 0, st>>>(m, s.pool, s.draw_j, s.head, s.link, s.stamp,
                                             out_batch, s.dval);
   SGDT_CUDA(cudaGetLastError());
   s.launches += 5;
   s.last_batch = out_batch;
   s.last_batch_len = m;
+  return SGDT_OK;
+}
+
+// row_fraction < 1 for one mode: per-row partial Fisher-Yates of every
+// bucket (a fresh copy each epoch, factor_optimizer.cpp:405-419), all rows'
+// draws from the session RNG in row order.  out[d] (d in row i's draw range
+// sub_off[i]..sub_off[i+1]) is the mode-order position of the kept entry.
+int launch_row_subsets(Session& s, int n, RowSubset& rs, cudaStream_t st) {
+  const uint64_t T = rs.total;
+  if (T == 0) return SGDT_OK;
+  if (++s.stamp == 0) {
+    SGDT_CUDA(cudaMemsetAsync(s.head, 0, s.nnz * sizeof(unsigned long long), st));
+    s.stamp = 1;
+  }
+  DrawPlan plan{};
+  plan.kind = 2;
+  plan.sub_off = rs.sub_off;
+  plan.n_rows = s.dims[n];
+  plan.row_ptr = s.mode[n].row_ptr;
+  plan.out_target = rs.target;
+  plan.out_pos = rs.pos;
+  mt_draw_kernel<<<1, 320, 0, st>>>(s.mt, T, plan);
+  SGDT_CUDA(cudaGetLastError());
+  const unsigned blocks = static_cast<unsigned>((T + 255) / 256);
+  link_kernel<<<blocks, 256, 0, st>>>(T, rs.target, s.head, s.stamp, rs.link);
+  resolve_kernel<<<blocks, 256, 0, st>>>(T, rs.target, rs.pos, s.head, rs.link, s.stamp, rs.kprev, rs.lprev);
+  chain_kernel<<<blocks, 256, 0, st>>>(T, nullptr, rs.pos, rs.target, rs.kprev, rs.lprev, nullptr, rs.out);
+  SGDT_CUDA(cudaGetLastError());
+  s.launches += 4;
   return SGDT_OK;
 }
 
@@ -241,7 +313,11 @@ extern "C" int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const ui
   h_state[kMtN] = pos;
   SGDT_CUDA(cudaMemcpy(d_state, h_state, sizeof h_state, cudaMemcpyHostToDevice));
   SGDT_CUDA(cudaMemcpy(d_bounds, bounds, n * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  mt_draw_kernel<1><<<1, 320>>>(d_state, n, 0, d_bounds, nullptr, d_out);
+  DrawPlan plan{};
+  plan.kind = 1;
+  plan.bounds = d_bounds;
+  plan.out64 = d_out;
+  mt_draw_kernel<<<1, 320>>>(d_state, n, plan);
   SGDT_CUDA(cudaGetLastError());
   SGDT_CUDA(cudaMemcpy(out, d_out, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   SGDT_CUDA(cudaMemcpy(h_state, d_state, sizeof h_state, cudaMemcpyDeviceToHost));

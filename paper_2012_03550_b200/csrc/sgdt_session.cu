@@ -53,6 +53,20 @@ __global__ void gather_mode_copy_kernel(const uint32_t* __restrict__ src_idx,
   }
 }
 
+// Kept records of a row-subset epoch: record q is the mode-order record at
+// position out[q] (the mode copy holds `len` records).
+__global__ void gather_subset_kernel(const uint32_t* __restrict__ src_idx, const float* __restrict__ src_val,
+                                     uint64_t len, const uint32_t* __restrict__ out, uint64_t T, int order,
+                                     uint32_t* idx, float* val) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < T;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = out[q];
+    for (int k = 0; k < order; ++k)
+      idx[static_cast<uint64_t>(k) * T + q] = src_idx[static_cast<uint64_t>(k) * len + p];
+    val[q] = src_val[p];
+  }
+}
+
 __global__ void cast_d2f_kernel(const double* __restrict__ src, float* dst, uint64_t n) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -242,6 +256,11 @@ void free_session(sgdt_session* s) {
     F(s->mode[n].row_ptr);
     F(s->mode[n].chunks);
     F(s->mode[n].splits);
+    RowSubset& rs = s->mode[n].subset;
+    for (void* p : {(void*)rs.sub_off, (void*)rs.target, (void*)rs.pos, (void*)rs.link, (void*)rs.kprev,
+                    (void*)rs.lprev, (void*)rs.out, (void*)rs.rec.idx, (void*)rs.rec.val, (void*)rs.chunks,
+                    (void*)rs.splits})
+      F(p);
     F(s->P.A[n]);
     F(s->P.B[n]);
     F(s->P.Q[n]);
@@ -342,8 +361,6 @@ int check_factor_hyper(const sgdt_factor_hyper* h) {
     return fail(SGDT_ERR_DOMAIN, "row fraction must lie in (0,1]");
   if (h->lr < 0.0) return fail(SGDT_ERR_DOMAIN, "factor learning rate must be non-negative");
   if (h->lr > 0.0 && h->reg < 0.0) return fail(SGDT_ERR_DOMAIN, "sgd_step: regularization must be non-negative");
-  if (h->lr > 0.0 && h->row_fraction < 1.0)
-    return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not implemented on the device path yet");
   return SGDT_OK;
 }
 
@@ -377,11 +394,81 @@ int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_
   return launch_core(s, h, batch, m, per_mode ? 1 : 0);
 }
 
+// The row-subset plan of mode n for `fraction`: keep_i = max(1,
+// llround(f |bucket_i|)) per non-empty row (factor_optimizer.cpp:409-411), the
+// subset row offsets and its chunk schedule.  Rebuilt only when f changes.
+int ensure_subset(Session& s, int n, double fraction) {
+  RowSubset& rs = s.mode[n].subset;
+  if (rs.fraction == fraction) return SGDT_OK;
+  SGDT_CUDA(cudaStreamSynchronize(s.stream));
+  const std::vector<uint64_t>& off = s.h_row_ptr[n];
+  std::vector<uint64_t> sub(off.size(), 0);
+  for (size_t i = 0; i + 1 < off.size(); ++i) {
+    const uint64_t bs = off[i + 1] - off[i];
+    uint64_t keep = 0;
+    if (bs) keep = std::max<uint64_t>(1, static_cast<uint64_t>(std::llround(fraction * static_cast<double>(bs))));
+    sub[i + 1] = sub[i] + keep;
+  }
+  const uint64_t T = sub.back();
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  for (void* p : {(void*)rs.sub_off, (void*)rs.target, (void*)rs.pos, (void*)rs.link, (void*)rs.kprev,
+                  (void*)rs.lprev, (void*)rs.out, (void*)rs.rec.idx, (void*)rs.rec.val, (void*)rs.chunks,
+                  (void*)rs.splits})
+    F(p);
+  rs = RowSubset{};
+  rs.total = T;
+  std::vector<uint32_t> sub32(sub.begin(), sub.end());
+  TRY(dalloc(&rs.sub_off, sub32.size()));
+  SGDT_CUDA(cudaMemcpy(rs.sub_off, sub32.data(), sub32.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  for (uint32_t** p : {&rs.target, &rs.pos, &rs.link, &rs.kprev, &rs.lprev, &rs.out}) TRY(dalloc(p, T));
+  rs.rec.nnz = T;
+  TRY(dalloc(&rs.rec.idx, T * s.order));
+  TRY(dalloc(&rs.rec.val, T));
+  std::vector<Chunk> chunks;
+  std::vector<SplitRow> splits;
+  ShardPlan sp;
+  build_chunks(sub, 0, T, s.chunk_size, chunks, splits, rs.n_pieces, sp);
+  rs.n_chunks = static_cast<uint32_t>(chunks.size());
+  rs.n_splits = static_cast<uint32_t>(splits.size());
+  TRY(dalloc(&rs.chunks, chunks.size()));
+  TRY(dalloc(&rs.splits, splits.size()));
+  if (!chunks.empty())
+    SGDT_CUDA(cudaMemcpy(rs.chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  if (!splits.empty())
+    SGDT_CUDA(cudaMemcpy(rs.splits, splits.data(), splits.size() * sizeof(SplitRow), cudaMemcpyHostToDevice));
+  if (rs.n_pieces > s.piece_cap) {
+    F(s.piece_partials);
+    s.piece_cap = rs.n_pieces;
+    TRY(dalloc(&s.piece_partials, static_cast<uint64_t>(s.piece_cap) * s.RP));
+  }
+  rs.fraction = fraction;
+  return SGDT_OK;
+}
+
 int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
   if (h.lr == 0.0) return SGDT_OK;
+  const bool subset = h.row_fraction < 1.0;
+  if (subset && s.world > 1)
+    return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not supported by the sharded (multi-GPU) factor phase");
   for (int n = 0; n < s.order; ++n) {
     if (time_modes) SGDT_CUDA(cudaEventRecord(s.ev[4 + n], s.stream));
-    TRY(launch_factor_mode(s, n, h));
+    if (subset) {
+      // the draws of mode n follow mode n-1's update in the RNG stream
+      // (factor_optimizer.cpp:384-424); they do not depend on the model.
+      TRY(ensure_subset(s, n, h.row_fraction));
+      RowSubset& rs = s.mode[n].subset;
+      TRY(launch_row_subsets(s, n, rs, s.stream));
+      if (rs.total) {
+        gather_subset_kernel<<<grid_for(rs.total, s.num_sms), 256, 0, s.stream>>>(
+            s.mode[n].rec.idx, s.mode[n].rec.val, s.mode[n].rec.nnz, rs.out, rs.total, s.order, rs.rec.idx,
+            rs.rec.val);
+        SGDT_CUDA(cudaGetLastError());
+        ++s.launches;
+      }
+    }
+    TRY(launch_factor_mode(s, n, h, subset));
   }
   return SGDT_OK;
 }
@@ -509,6 +596,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
             s->train_rec.idx, s->train_rec.val, d_perm, s->nnz, len, s->order, mp.rec.idx, mp.rec.val);
         SGDT_CUDA(cudaGetLastError());
       }
+      s->h_row_ptr[n] = off;
       std::vector<uint32_t> rp(off.size());
       for (size_t i = 0; i < off.size(); ++i) rp[i] = static_cast<uint32_t>(off[i]);
       TRY(dalloc(&mp.row_ptr, rp.size()));
@@ -552,7 +640,8 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     }
     TRY(dalloc(&s->stage, stage));
     s->stage_cap = stage;
-    TRY(dalloc(&s->piece_partials, static_cast<uint64_t>(std::max<uint32_t>(max_pieces, 1)) * s->RP));
+    s->piece_cap = std::max<uint32_t>(max_pieces, 1);
+    TRY(dalloc(&s->piece_partials, static_cast<uint64_t>(s->piece_cap) * s->RP));
     TRY(dalloc(&s->export_buf, 2ull * s->RP));
     // sampler
     TRY(dalloc(&s->mt, 313));
@@ -736,7 +825,8 @@ int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
   // stream during epoch e's factor phase (double-buffered Psi).  The RNG
   // stream is consumed in exactly the reference order: the factor phase draws
   // nothing (row_fraction == 1).
-  const bool ahead = ch->lr > 0.0 && ch->batch_m != 0;
+  // (with row_fraction < 1 the factor phase also draws, so no run-ahead)
+  const bool ahead = ch->lr > 0.0 && ch->batch_m != 0 && !(fh->lr > 0.0 && fh->row_fraction < 1.0);
   uint32_t* buf[2] = {nullptr, nullptr};
   if (ahead) {
     TRY(ensure_batch_capacity(*s, m));
@@ -825,6 +915,8 @@ int sgdt_factor_mode_local(sgdt_session* s, int mode, const sgdt_factor_hyper* h
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_mode_local: mode out of range");
   TRY(check_factor_hyper(h));
+  if (h->lr > 0.0 && h->row_fraction < 1.0)
+    return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not supported by the sharded (multi-GPU) factor phase");
   SGDT_CUDA(cudaSetDevice(s->device));
   if (h->lr == 0.0) return SGDT_OK;
   TRY(launch_factor_mode(*s, mode, *h));

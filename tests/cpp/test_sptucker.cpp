@@ -203,6 +203,30 @@ void test_epochs_teacher_forced(std::vector<std::uint32_t> dims, std::vector<std
   or_core_ws_free(&ows);
 }
 
+void test_row_fraction() {
+  const std::vector<std::uint32_t> dims{6, 80, 50}, J{4, 4, 4};
+  const double sig = unit_sigma(3, 4, 4);
+  const Data d = planted(dims, J, 4, 4000, 0.05, 0.0, sig, 3);
+  const CooTensor t = to_tensor(d);
+  OTensor ot(d);
+  TuckerModel tm = TuckerModel::init_gaussian(t.shape(), Ranks{J, 4}, 0.0, sig, 12);
+  OModel om(dims, J, 4);
+  sync_f32(tm, om);
+  Rng rng(31);
+  or_rng orng;
+  copy_rng(rng, orng);
+  std::vector<RowBatchWorkspace> rws;
+  SchedContext sched;
+  for (const double f : {0.5, 0.25}) {
+    update_factor_epoch(tm, t, FactorHyper{0.02, 0.01, f}, sched, rng, rws);
+    const or_factor_hyper h{0.02, 0.01, f};
+    CHECK(or_update_factor_epoch(&om.m, &ot.t, &h, &orng, nullptr, nullptr) == 0);
+    CHECK(same_rng(rng, orng));
+    CHECK(max_rel(tm, om, true) <= 1e-4);
+    sync_f32(tm, om);
+  }
+}
+
 void test_rmse_fixed_and_perfect() {
   // zero model, values {0, 2}: RMSE sqrt(2), MAE 1 (test_eval.cpp:32-41)
   const CooTensor t(Shape({2, 1}), {1, 1, 2, 1}, {0.0, 2.0});
@@ -355,6 +379,7 @@ int main(int argc, char** argv) {
   run("epochs order-2", [] { test_epochs_teacher_forced({30, 25}, {3, 3}, 3, 220, 20, false); });
   run("epochs split rows", [] { test_epochs_teacher_forced({6, 300, 300}, {8, 8, 8}, 8, 30000, 2048, false); });
   run("epochs R10", [] { test_epochs_teacher_forced({50, 40, 30}, {10, 10, 10}, 10, 8000, 1024, false); });
+  run("row fraction", test_row_fraction);
   run("rmse", test_rmse_fixed_and_perfect);
   run("freeze and errors", test_freeze_and_errors);
   run("train end to end", test_train_end_to_end_vs_oracle);

@@ -326,3 +326,59 @@ def test_run_epochs_pipelined_sampler_matches_oracle():
         RA, RB = m.params()
         for n in range(3):
             assert rel_err(A[n], RA[n]) <= TOL and rel_err(B[n], RB[n]) <= TOL
+
+
+@pytest.mark.parametrize("fraction,chunk", [(0.5, None), (0.3, "64"), (0.999, None), (0.05, "40")])
+def test_row_fraction_subsets(monkeypatch, fraction, chunk):
+    """row_fraction < 1 (factor_optimizer.cpp:143-165): every row's subset is
+    a partial Fisher-Yates of its bucket drawn from the session RNG in row
+    order -- the draws must consume exactly the reference's outputs -- and the
+    step uses the kept entries with |subset| as the batch count."""
+    if chunk:
+        monkeypatch.setenv("SGDT_CHUNK_SIZE", chunk)
+    dims, J, R = (6, 80, 50), (4, 4, 4), 4
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, R, 4000, 3, tm=0.0, ts=sig)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 12, sd=sig, mean=0.0)
+    rng = O.Rng(31)
+    s.set_rng(*rng.state())
+    for epoch in range(2):
+        s.set_model(*m.params())
+        up, sk = s.factor_epoch(0.02, 0.01, fraction)
+        rup, rsk = O.update_factor_epoch(m, t, 0.02, 0.01, rng, fraction)
+        assert (up, sk) == (rup, rsk)
+        st, pos = s.get_rng()
+        rst, rpos = rng.state()
+        assert pos == rpos and np.array_equal(st, rst)
+        A, _ = s.get_model()
+        RA, RB = m.params()
+        for n in range(3):
+            assert rel_err(A[n], RA[n]) <= TOL, f"epoch {epoch} mode {n}"
+        m.set_params([f32(a) for a in RA], [f32(b) for b in RB])
+
+
+def test_row_fraction_in_run_epochs_matches_oracle():
+    dims, J, R = (20, 30, 25), (3, 3, 3), 3
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, R, 5000, 8, tm=0.0, ts=sig)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 2, sd=sig, mean=0.0)
+    s.set_model(*m.params())
+    rng = O.Rng(6)
+    ws = O.CoreWorkspace(5000)
+    s.set_rng(*rng.state())
+    s.run_epochs(sg().CoreHyper(0.01, 0.01, 300, 0, 0), sg().FactorHyper(0.01, 0.01, 0.6), 3)
+    for _ in range(3):
+        O.update_core_epoch(m, t, 0.01, 0.01, 300, rng, ws)
+        O.update_factor_epoch(m, t, 0.01, 0.01, rng, 0.6)
+    st, pos = s.get_rng()
+    rst, rpos = rng.state()
+    assert pos == rpos and np.array_equal(st, rst)
+    assert np.array_equal(s.last_batch(), ws.batch())
+    A, B = s.get_model()
+    RA, RB = m.params()
+    for n in range(3):
+        assert rel_err(A[n], RA[n]) <= TOL and rel_err(B[n], RB[n]) <= TOL
