@@ -45,6 +45,8 @@ struct CoreArgs {
   double lr, reg;
   int* flag;
   int q_refresh;      // fuse Q = A B for every mode at the end
+  int local;          // per-sample state of the CTA's slice lives in shared memory
+  uint32_t cap;       // samples per CTA slice (upper bound)
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -81,15 +83,30 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
   const uint64_t base = a.m / gridDim.x, rem = a.m % gridDim.x;
   const uint64_t s0 = blockIdx.x * base + (blockIdx.x < rem ? blockIdx.x : rem);
   const uint64_t s1 = s0 + base + (blockIdx.x < rem ? 1 : 0);
+  const uint32_t nloc = static_cast<uint32_t>(s1 - s0);
   const double inv_m = 1.0 / static_cast<double>(a.m);
+  // per-sample state of this slice (local index ls = s - s0): shared memory
+  // when it fits, else the global scratch
+  float *la, *lc, *lxh, *lx;
+  if (a.local) {
+    la = dbv + a.js;
+    lc = la + static_cast<uint64_t>(a.cap) * a.js;
+    lxh = lc + static_cast<uint64_t>(a.cap) * RP;
+    lx = lxh + a.cap;
+  } else {
+    la = a.sa + s0 * a.js;
+    lc = a.sc + s0 * RP;
+    lxh = a.sxh + s0;
+    lx = a.sx + s0;
+  }
   uint32_t step = 0;
 
   for (int n = 0; n < a.P.order; ++n) {
     const uint32_t* batch = a.batch + (a.per_mode ? static_cast<uint64_t>(n) * a.m : 0);
     const uint32_t jn = a.P.J[n];
     // ---- per-sample caches: c_{s,r}, a_s, xhat_s, x_s  (:158-180)
-    for (uint64_t s = s0 + tid; s < s1; s += blockDim.x) {
-      const uint32_t e = batch[s];
+    for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
+      const uint32_t e = batch[s0 + ls];
       float c[RP];
 #pragma unroll
       for (int r = 0; r < RP; ++r) c[r] = 1.f;
@@ -115,7 +132,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
       for (int r = 0; r < RP; ++r) p[r] = 0.f;
       for (uint32_t j = 0; j < jn; ++j) {
         const float av = arow[j];
-        a.sa[s * a.js + j] = av;
+        la[ls * a.js + j] = av;
 #pragma unroll
         for (int r = 0; r < RP; ++r) p[r] = fmaf(av, bs[n][j * RP + r], p[r]);
       }
@@ -123,10 +140,10 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
         xh = fmaf(c[r], p[r], xh);
-        a.sc[s * RP + r] = c[r];
+        lc[ls * RP + r] = c[r];
       }
-      a.sxh[s] = xh;
-      a.sx[s] = a.rec_val[e];
+      lxh[ls] = xh;
+      lx[ls] = a.rec_val[e];
     }
     __syncthreads();
 
@@ -137,9 +154,9 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
         // thread-per-sample terms, warp reduction per j (fixed order)
         for (uint32_t j = 0; j < jn; ++j) {
           float v = 0.f;
-          for (uint64_t s = s0 + tid; s < s1; s += blockDim.x) {
-            const float t = a.sc[s * RP + rc] * (a.sxh[s] - a.sx[s]);
-            v = fmaf(t, a.sa[s * a.js + j], v);
+          for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
+            const float t = lc[ls * RP + rc] * (lxh[ls] - lx[ls]);
+            v = fmaf(t, la[ls * a.js + j], v);
           }
           v = warp_sum(v);
           if (lane == 0) wpart[warp * a.js + j] = static_cast<double>(v);
@@ -148,32 +165,38 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
         if (tid < static_cast<int>(jn)) {
           double acc = 0.0;
           for (int w = 0; w < nwarps; ++w) acc += wpart[w * a.js + tid];
-          part[static_cast<uint64_t>(blockIdx.x) * a.js + tid] = acc;
+          part[static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x] = acc;  // [j][cta]
         }
       }
       grid.sync();
-      // ---- every CTA: V in CTA order, sgd_step on column rc (identical everywhere)
-      if (tid < static_cast<int>(jn)) {
+      // ---- every CTA: V_j over the CTA partials (a warp per j, fixed lane
+      // striding + butterfly, so every CTA forms the identical sum), then
+      // sgd_step on column rc
+      for (uint32_t j = warp; j < jn; j += nwarps) {
+        const double* pj = part + static_cast<uint64_t>(j) * gridDim.x;
         double V = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b)
-          V += __ldcg(part + static_cast<uint64_t>(b) * a.js + tid);
-        const float bold = bs[n][tid * RP + rc];
-        double w = static_cast<double>(bold);
-        int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
-        w -= a.lr * (V * inv_m + a.reg * w);
-        const float bnew = static_cast<float>(w);
-        bad |= !isfinite(bnew) ? 4 : 0;
-        if (bad && blockIdx.x == 0) atomicOr(a.flag, bad);
-        dbv[tid] = bnew - bold;
-        bs[n][tid * RP + rc] = bnew;
+        for (unsigned b = lane; b < gridDim.x; b += 32) V += __ldcg(pj + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) V += __shfl_xor_sync(0xffffffffu, V, o);
+        if (lane == 0) {
+          const float bold = bs[n][j * RP + rc];
+          double w = static_cast<double>(bold);
+          int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
+          w -= a.lr * (V * inv_m + a.reg * w);
+          const float bnew = static_cast<float>(w);
+          bad |= !isfinite(bnew) ? 4 : 0;
+          if (bad && blockIdx.x == 0) atomicOr(a.flag, bad);
+          dbv[j] = bnew - bold;
+          bs[n][j * RP + rc] = bnew;
+        }
       }
       __syncthreads();
       // ---- keep xhat current for the next column
       if (rc + 1 < a.P.R) {
-        for (uint64_t s = s0 + tid; s < s1; s += blockDim.x) {
+        for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
           float d = 0.f;
-          for (uint32_t j = 0; j < jn; ++j) d = fmaf(a.sa[s * a.js + j], dbv[j], d);
-          a.sxh[s] = fmaf(a.sc[s * RP + rc], d, a.sxh[s]);
+          for (uint32_t j = 0; j < jn; ++j) d = fmaf(la[ls * a.js + j], dbv[j], d);
+          lxh[ls] = fmaf(lc[ls * RP + rc], d, lxh[ls]);
         }
         __syncthreads();
       }
@@ -239,15 +262,9 @@ int core_launch_rp(Session& s, CoreArgs& a) {
   const int block = 256;
   size_t bs_floats = 0;
   for (int k = 0; k < s.order; ++k) bs_floats += s.J[k] * RP;
-  const size_t smem = ((bs_floats + 1) & ~size_t(1)) * sizeof(float) +
-                      (block / 32) * a.js * sizeof(double) + a.js * sizeof(float);
+  size_t smem = ((bs_floats + 1) & ~size_t(1)) * sizeof(float) + (block / 32) * a.js * sizeof(double) +
+                a.js * sizeof(float);
   auto kern = core_kernel<RP>;
-  if (smem > 48 * 1024)
-    SGDT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  int per_sm = 0;
-  SGDT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
-  if (per_sm < 1) return fail(SGDT_ERR_INTERNAL, "core kernel does not fit on an SM");
   // one CTA per SM keeps grid.sync cheap; small batches use fewer CTAs
   uint64_t want = (a.m + 127) / 128;
   if (want < 1) want = 1;
@@ -257,6 +274,15 @@ int core_launch_rp(Session& s, CoreArgs& a) {
     for (int k = 0; k < s.order; ++k) rows += s.dims[k];
     if (rows > static_cast<uint64_t>(grid) * block * 8) grid = s.num_sms;
   }
+  a.cap = static_cast<uint32_t>((a.m + grid - 1) / grid);
+  const size_t local = static_cast<size_t>(a.cap) * (a.js + RP + 2) * sizeof(float);
+  a.local = smem + local <= 200 * 1024;
+  if (a.local) smem += local;
+  if (smem > 48 * 1024)
+    SGDT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  SGDT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
+  if (per_sm < 1) return fail(SGDT_ERR_INTERNAL, "core kernel does not fit on an SM");
   s.core_grid = grid;
   void* args[] = {&a};
   SGDT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(block),

@@ -125,6 +125,44 @@ __device__ __forceinline__ void finalize_row(const FactorArgs& a, const float* b
   finalize_row_impl<RP>(row_update(a, bsn), row, gf);
 }
 
+// The same row update done by the whole warp: g (held by lane `src`) is
+// broadcast, lane j updates a_j, lane r rebuilds Q^(n)[row][r].  ~RP + J
+// shuffles instead of ~J*RP serial FMAs on one lane.
+template <int RP>
+__device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const float* bsn, uint32_t row,
+                                                  const float (&g)[RP], int src, uint32_t lane) {
+  float gg[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) gg[r] = __shfl_sync(0xffffffffu, g[r], src);
+  const uint32_t jn = a.P.J[a.n];
+  const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
+  const float inv = 1.0f / static_cast<float>(cnt);
+  const float lr = static_cast<float>(a.lr), reg = static_cast<float>(a.reg);
+  float* arow = a.P.A[a.n] + static_cast<uint64_t>(row) * jn;
+  int bad = 0;
+  float q = 0.f;
+  for (uint32_t j0 = 0; j0 < jn; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    float wn = 0.f;
+    if (j < jn) {
+      float F = 0.f;
+#pragma unroll
+      for (int r = 0; r < RP; ++r) F = fmaf(bsn[j * RP + r], gg[r], F);
+      const float w = arow[j];
+      wn = w - lr * fmaf(F, inv, reg * w);
+      bad |= !isfinite(w) || !isfinite(F) || !isfinite(wn);
+      arow[j] = wn;
+    }
+    const uint32_t jend = jn - j0 < 32 ? jn - j0 : 32;
+    for (uint32_t t = 0; t < jend; ++t) {
+      const float aj = __shfl_sync(0xffffffffu, wn, t);
+      if (lane < RP) q = fmaf(aj, bsn[(j0 + t) * RP + lane], q);
+    }
+  }
+  if (lane < RP) a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
+}
+
 template <int RP, typename T>
 __device__ __forceinline__ void warp_allreduce(T (&x)[RP]) {
 #pragma unroll
@@ -240,6 +278,24 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
       continue;
     }
     // ---- window crosses a row boundary
+    const uint32_t pkey = __shfl_up_sync(kFull, key, 1);
+    const unsigned vmask = __ballot_sync(kFull, valid);
+    const unsigned heads = __ballot_sync(kFull, valid && (lane == 0 ? key != cur : key != pkey));
+    if (__popc(heads) == 1) {
+      // one row ends here (cur, lanes < b plus the carry) and one row starts
+      // at lane b and stays open: no scan, one warp reduction.
+      const int b = __ffs(heads) - 1;
+      float tot[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) tot[r] = acc[r] + (static_cast<int>(lane) < b ? v[r] : 0.f);
+      warp_allreduce<RP>(tot);
+      finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);
+      cur = __shfl_sync(kFull, key, b);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) acc[r] = static_cast<int>(lane) >= b ? v[r] : 0.f;
+      spread = true;
+      continue;
+    }
     float tot[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) tot[r] = acc[r];
@@ -261,17 +317,25 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
       }
     }
     const uint32_t nkey = __shfl_down_sync(kFull, key, 1);
-    const unsigned vmask = __ballot_sync(kFull, valid);
     const int last_valid = 31 - __clz(vmask);
     const bool seg_end = valid && (lane == 31 || nkey != key);
     const bool is_last = static_cast<int>(lane) == last_valid;
-    const bool first_seg = key == cur;
-    if (first_seg) {
+    if (key == cur) {
 #pragma unroll
       for (int r = 0; r < RP; ++r) v[r] += tot[r];
     }
-    if (lane == 0 && key != cur) finalize_row<RP>(a, bsn, cur, tot);  // row ended at the window edge
-    if (seg_end && !is_last) finalize_row<RP>(a, bsn, key, v);
+    const uint32_t key0 = __shfl_sync(kFull, key, 0);
+    unsigned fin = __ballot_sync(kFull, seg_end && !is_last);
+    if (key0 != cur) finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);  // row ended at the window edge
+    if (__popc(fin) <= 4) {
+      while (fin) {
+        const int src = __ffs(fin) - 1;
+        fin &= fin - 1;
+        finalize_row_warp<RP>(a, bsn, __shfl_sync(kFull, key, src), v, src, lane);
+      }
+    } else if (seg_end && !is_last) {
+      finalize_row<RP>(a, bsn, key, v);
+    }
     cur = __shfl_sync(kFull, key, last_valid);
 #pragma unroll
     for (int r = 0; r < RP; ++r) acc[r] = is_last ? v[r] : 0.f;
@@ -288,14 +352,12 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
 #pragma unroll
     for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, tot[r], carry_lane);
   }
-  if (lane == 0) {
-    if (ch.piece < 0) {
-      finalize_row<RP>(a, bsn, cur, tot);
-    } else {
-      double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
+  if (ch.piece < 0) {
+    finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);
+  } else if (lane == 0) {
+    double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
 #pragma unroll
-      for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(tot[r]);
-    }
+    for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(tot[r]);
   }
 }
 
