@@ -51,6 +51,19 @@ struct FactorArgs {
   int* flag;
 };
 
+// Streamed record loads: read once, never reused -> keep them out of L1,
+// which is reserved for the Q-row gathers that live on its hits.
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 template <int RP>
 __device__ __forceinline__ void load_bsn(const FactorArgs& a, float* bsn) {
   const uint32_t jn = a.P.J[a.n];
@@ -201,10 +214,10 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
   {
     const uint32_t e = ch.begin + lane;
     if (e < ch.end) {
-      pk = __ldcs(a.keys + e);
-      px = __ldcs(a.val + e);
+      pk = ld_stream(a.keys + e);
+      px = ld_stream(a.val + e);
 #pragma unroll
-      for (int j = 0; j < NO; ++j) pi[j] = __ldcs(a.oidx[j] + e);
+      for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
     }
   }
   uint32_t cur = __shfl_sync(kFull, pk, 0);
@@ -225,10 +238,10 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
       const uint32_t e = base + 32 + lane;
       pk = kNone;
       if (e < ch.end) {
-        pk = __ldcs(a.keys + e);
-        px = __ldcs(a.val + e);
+        pk = ld_stream(a.keys + e);
+        px = ld_stream(a.val + e);
 #pragma unroll
-        for (int j = 0; j < NO; ++j) pi[j] = __ldcs(a.oidx[j] + e);
+        for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
       }
     }
     float v[RP];
