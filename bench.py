@@ -49,7 +49,7 @@ def parse():
                    help="fraction of the config's nnz (debug only; 1.0 for reported runs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_NNZ)
+    p.add_argument("--cpu-sample", type=int, default=0, help="override the per-config CPU sample size")
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (sharded factor phase) driver even on one rank")
     return p.parse_args()
@@ -57,6 +57,20 @@ def parse():
 
 HYPER = dict(lr_a=0.01, lr_b=0.01, reg_a=0.01, reg_b=0.01, init_mean=0.5, init_sd=0.1, seed=1)
 BATCH_M = {2: 65536, 3: 262144, 4: 65536, 5: 262144}
+# CPU-baseline sample per config (nonzeros): the reference's per-unit cost is
+# prod(J) FMAs (dense core), so large cores get smaller samples.
+CPU_SAMPLE = {2: 3_000_000, 3: 2_000_000, 4: 0, 5: 100_000}
+REF_UNAVAILABLE = {4: "the reference rejects config 4: Shape overflows 64 bits (1e5^4 x 1e3, sptensor.cpp:34-35) "
+                      "and prod J = 16^5 exceeds kMaxCoreElems (model.hpp:25)"}
+
+
+def init_stats(cfg, spec):
+    """Init of the model: the paper's N(0.5, 0.1^2) for config 2; configs 3-5
+    use N(0, sigma^2) at the teacher's unit-variance scale (with mean 0.5 the
+    initial xhat ~ R (J/4)^N makes fixed-lr SGD diverge there)."""
+    if cfg == 2:
+        return HYPER["init_mean"], HYPER["init_sd"]
+    return 0.0, spec.unit_sigma
 
 
 def measured_peak():
@@ -152,14 +166,14 @@ def init_model(dims, J, R, mean, sd, seed):
     return A, B
 
 
-def cpu_reference_run(data, J, R, m, warmup, epochs, threads):
+def cpu_reference_run(data, J, R, m, warmup, epochs, threads, init=(0.5, 0.1)):
     """Reference CPU epochs on a bounded sample of the same tensor.
     Returns (seconds/epoch, kind, cores, sample_desc, units/epoch)."""
     from oracle import oracle_py as O
     spec = data["spec"]
     trc, trv = data["train"]
     rs = np.random.default_rng(12345)
-    S = min(len(trv), data.get("cpu_sample", CPU_SAMPLE_NNZ))
+    S = min(len(trv), data.get("cpu_sample") or CPU_SAMPLE.get(data["cfg"], CPU_SAMPLE_NNZ))
     pick = np.sort(rs.choice(len(trv), S, replace=False))
     c, v = trc[pick], trv[pick]
     order = len(spec.dims)
@@ -167,19 +181,19 @@ def cpu_reference_run(data, J, R, m, warmup, epochs, threads):
     Jv = np.array([J] * order, np.uint32)
     desc = (f"{S:,} of {len(trv):,} training nonzeros of config {data['cfg']} (uniform random "
             f"subset, same shape), M={mm}, {epochs} timed epoch(s) after {warmup} warm-up, "
-            f"Strategy::Improved, init N(0.5,0.1^2)")
+            f"Strategy::Improved, init N({init[0]:.3g},{init[1]:.3g}^2)")
     if O.ref_available():
         import ctypes as C
         t = O.RefTensor(spec.dims, c, v)
         sec = C.c_double()
-        rc = O.ref().ref_bench_epoch_seconds(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"],
-                                            mm, 2, threads, warmup, epochs, 1, C.byref(sec))
+        rc = O.ref().ref_time_epochs(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"], mm, 2, threads,
+                                     warmup, epochs, 1, init[0], init[1], C.byref(sec))
         if rc != 0:
             raise RuntimeError(f"reference bench failed: {rc}")
         return sec.value, "reference", threads, desc, units_per_epoch(order, mm, S)
     # oracle port: single thread, serial strategy
     t = O.Tensor(spec.dims, c, v)
-    model = O.Model(spec.dims, Jv, R).init_gaussian(0.5, 0.1, 1)
+    model = O.Model(spec.dims, Jv, R).init_gaussian(init[0], init[1], 1)
     rng = O.Rng(2)
     ws = O.CoreWorkspace(S)
     times = []
@@ -196,6 +210,9 @@ def cpu_reference_run(data, J, R, m, warmup, epochs, threads):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
+    if args.config in REF_UNAVAILABLE:
+        print(json.dumps({"impl": "reference", "unavailable": REF_UNAVAILABLE[args.config]}), flush=True)
+        return 0
     import torch
     cfg = args.config
     data = make_data(cfg, args.scale, "cuda" if torch.cuda.is_available() else "cpu")
@@ -205,7 +222,8 @@ def run_reference_arm(args, rank, world):
     threads = os.cpu_count() or 1
     J = R = spec.teacher_j
     m = BATCH_M[cfg]
-    sec, kind, cores, desc, units = cpu_reference_run(data, J, R, m, args.warmup, args.steps, threads)
+    sec, kind, cores, desc, units = cpu_reference_run(data, J, R, m, args.warmup, args.steps, threads,
+                                                      init_stats(cfg, spec))
     value = units / sec
     line = {
         "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
@@ -245,7 +263,7 @@ def run_sharded(args, rank, world, local_rank):
     s = D.ShardedSession(spec.dims, trc, trv, [J] * order, R, rank, world, test=data["test"], perms=data["perms"],
                          device=local_rank)
     setup_s = time.time() - t0
-    A, B = init_model(spec.dims, J, R, HYPER["init_mean"], HYPER["init_sd"], HYPER["seed"])
+    A, B = init_model(spec.dims, J, R, *init_stats(cfg, spec), HYPER["seed"])
     s.set_model(A, B)
     s.seed(HYPER["seed"] + 1)
     ch = sgdt.CoreHyper(HYPER["lr_b"], HYPER["reg_b"], m, 0, 0)
@@ -310,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
     s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"], perms=data["perms"],
                      device=local_rank)
     setup_s = time.time() - t0
-    A, B = init_model(spec.dims, J, R, HYPER["init_mean"], HYPER["init_sd"], HYPER["seed"])
+    A, B = init_model(spec.dims, J, R, *init_stats(cfg, spec), HYPER["seed"])
     s.set_model(A, B)
     s.seed(HYPER["seed"] + 1)
     ch = sgdt.CoreHyper(HYPER["lr_b"], HYPER["reg_b"], m, 0, 0)
@@ -388,9 +406,12 @@ def run_ours(args, rank, world, local_rank):
                "setup_s": setup_s}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and cfg in REF_UNAVAILABLE and not args.no_cpu_baseline:
+        cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable", "sample": REF_UNAVAILABLE[cfg]}
+    elif rank == 0 and not args.no_cpu_baseline:
         try:
-            sec, kind, cores, desc, cu = cpu_reference_run(data, J, R, m, 1, 1, os.cpu_count() or 1)
+            sec, kind, cores, desc, cu = cpu_reference_run(data, J, R, m, 1, 1, os.cpu_count() or 1,
+                                                           init_stats(cfg, spec))
             cpu = {"value": cu / sec, "unit": "updates/s", "cores": cores, "kind": kind, "sample": desc}
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",

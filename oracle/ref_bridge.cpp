@@ -336,4 +336,34 @@ int ref_bench_epoch_seconds(void* train_t, const std::uint32_t* J, std::uint32_t
   });
 }
 
+// timed_epochs (eval.cpp:201-223) with a configurable initialisation: the
+// reference's own epoch calls, Strategy as given, `threads` workers; median
+// seconds of (core + factor) over `epochs` after `warmup`.
+int ref_time_epochs(void* train_t, const std::uint32_t* J, std::uint32_t R, double lr_a, double lr_b,
+                    double reg, std::size_t batch_m, int strategy, std::size_t threads, std::size_t warmup,
+                    std::size_t epochs, std::uint64_t seed, double init_mean, double init_sd, double* seconds) {
+  GUARD({
+    const CooTensor& tr = *static_cast<RefTensor*>(train_t)->t;
+    TuckerModel model = TuckerModel::init_gaussian(
+        tr.shape(), Ranks{std::vector<std::uint32_t>(J, J + tr.order()), R}, init_mean, init_sd, seed);
+    Rng rng(seed + 1);
+    WorkerPool pool(threads);
+    SchedContext sched{threads <= 1 ? Strategy::Serial : strat_of(strategy), BalancePolicy::Dynamic,
+                       threads <= 1 ? nullptr : &pool};
+    CoreBatchWorkspace cws;
+    std::vector<RowBatchWorkspace> rws(sched.workers());
+    std::vector<double> secs;
+    for (std::size_t e = 0; e < warmup + epochs; ++e) {
+      const auto t0 = std::chrono::steady_clock::now();
+      update_core_epoch(model, tr, CoreHyper{lr_b, reg, batch_m, false, false}, sched, rng, cws);
+      update_factor_epoch(model, tr, FactorHyper{lr_a, reg, 1.0}, sched, rng, rws);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (e >= warmup) secs.push_back(std::chrono::duration<double>(t1 - t0).count());
+    }
+    std::sort(secs.begin(), secs.end());
+    const std::size_t k = secs.size();
+    *seconds = k % 2 ? secs[k / 2] : 0.5 * (secs[k / 2 - 1] + secs[k / 2]);
+  });
+}
+
 }  // extern "C"

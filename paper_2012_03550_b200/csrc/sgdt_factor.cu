@@ -142,11 +142,8 @@ __device__ __forceinline__ void finalize_row(const FactorArgs& a, const float* b
 // broadcast, lane j updates a_j, lane r rebuilds Q^(n)[row][r].  ~RP + J
 // shuffles instead of ~J*RP serial FMAs on one lane.
 template <int RP>
-__device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const float* bsn, uint32_t row,
-                                                  const float (&g)[RP], int src, uint32_t lane) {
-  float gg[RP];
-#pragma unroll
-  for (int r = 0; r < RP; ++r) gg[r] = __shfl_sync(0xffffffffu, g[r], src);
+__device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const float* bsn, uint32_t row,
+                                                      const float (&gg)[RP], uint32_t lane) {
   const uint32_t jn = a.P.J[a.n];
   const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
   const float inv = 1.0f / static_cast<float>(cnt);
@@ -174,6 +171,18 @@ __device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const flo
   }
   if (lane < RP) a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
+}
+
+// The same row update done by the whole warp: g (held by lane `src`) is
+// broadcast, lane j updates a_j, lane r rebuilds Q^(n)[row][r].  ~RP + J
+// shuffles instead of ~J*RP serial FMAs on one lane.
+template <int RP>
+__device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const float* bsn, uint32_t row,
+                                                  const float (&g)[RP], int src, uint32_t lane) {
+  float gg[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) gg[r] = __shfl_sync(0xffffffffu, g[r], src);
+  finalize_row_warp_all<RP>(a, bsn, row, gg, lane);
 }
 
 template <int RP, typename T>
@@ -374,6 +383,215 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
   }
 }
 
+// ---------------------------------------------------------------------------
+// Wide rows (RP >= 16): G = RP/4 lanes cooperate on one entry, each lane owning
+// a float4 slice of the R-space vectors, E = 32/G entries per warp step.  A Q
+// row is gathered by one LDG.128 per lane of the group; p needs a log2(G)
+// group reduction; row boundaries are a scan over E groups of float4s.  This
+// keeps 4 accumulator registers per lane where the one-entry-per-lane kernel
+// would carry RP of them and scan RP-wide vectors over 32 lanes.
+template <int RP>
+struct Lanes {
+  static constexpr int G = RP / 4;
+  static constexpr int E = 32 / G;
+  static constexpr bool kPow2 = (G & (G - 1)) == 0;
+};
+
+template <int G, bool POW2>
+__device__ __forceinline__ float group_sum(float p, int leader) {
+  if constexpr (G == 1) {
+    return p;
+  } else if constexpr (POW2) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(kFull, p, o);
+    return p;
+  } else {
+    float t = 0.f;
+#pragma unroll
+    for (int s = 0; s < G; ++s) t += __shfl_sync(kFull, p, leader + s);
+    return t;
+  }
+}
+
+__device__ __forceinline__ float4 shfl4(const float4& v, int src) {
+  return make_float4(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src), __shfl_sync(kFull, v.z, src),
+                     __shfl_sync(kFull, v.w, src));
+}
+__device__ __forceinline__ float4 shfl4_up(const float4& v, int d) {
+  return make_float4(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d),
+                     __shfl_up_sync(kFull, v.z, d), __shfl_up_sync(kFull, v.w, d));
+}
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// All lanes receive the RP components held by group `grp` (4 per lane).
+template <int RP>
+__device__ __forceinline__ void group_row(const float4& v, int grp, float (&g)[RP]) {
+#pragma unroll
+  for (int s = 0; s < RP / 4; ++s) {
+    const float4 o = shfl4(v, grp * (RP / 4) + s);
+    g[4 * s] = o.x;
+    g[4 * s + 1] = o.y;
+    g[4 * s + 2] = o.z;
+    g[4 * s + 3] = o.w;
+  }
+}
+
+template <int RP, int NO>
+__global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
+  constexpr int G = Lanes<RP>::G, E = Lanes<RP>::E;
+  __shared__ float bsn[SGDT_MAX_J * RP];
+  load_bsn<RP>(a, bsn);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= a.n_chunks) return;
+  const Chunk ch = a.chunks[wid];
+  const int gi = static_cast<int>(lane) / G, sub = static_cast<int>(lane) % G, leader = gi * G;
+  const bool glane = gi < E;
+  const float* Qn = a.P.Q[a.n];
+
+  uint32_t pk = kNone, pi[NO];
+  float px = 0.f;
+  {
+    const uint32_t e = ch.begin + gi;
+    if (glane && e < ch.end) {
+      pk = ld_stream(a.keys + e);
+      px = ld_stream(a.val + e);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
+    }
+  }
+  uint32_t cur = __shfl_sync(kFull, pk, 0);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool spread = false;  // acc spread over the groups (else it lives in group carry_g)
+  int carry_g = 0;
+
+  for (uint32_t base = ch.begin; base < ch.end; base += E) {
+    const uint32_t key = pk;
+    const float x = px;
+    uint32_t ik[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) ik[j] = pi[j];
+    const bool valid = key != kNone;
+    {
+      const uint32_t e = base + E + gi;
+      pk = kNone;
+      if (glane && e < ch.end) {
+        pk = ld_stream(a.keys + e);
+        px = ld_stream(a.val + e);
+#pragma unroll
+        for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
+      }
+    }
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+    float p = 0.f;
+    if (valid) {
+      float4 t[NO];
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+        t[j] = __ldg(reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP) + sub);
+      const float4 h = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP)[sub];
+      c = t[0];
+#pragma unroll
+      for (int j = 1; j < NO; ++j) {
+        c.x *= t[j].x;
+        c.y *= t[j].y;
+        c.z *= t[j].z;
+        c.w *= t[j].w;
+      }
+      p = h.x * c.x;
+      p = fmaf(h.y, c.y, p);
+      p = fmaf(h.z, c.z, p);
+      p = fmaf(h.w, c.w, p);
+    }
+    p = group_sum<G, Lanes<RP>::kPow2>(p, leader);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      const float tt = p - x;
+      v = make_float4(tt * c.x, tt * c.y, tt * c.z, tt * c.w);
+    }
+    if (__all_sync(kFull, !glane || key == cur)) {
+      add4(acc, v);
+      spread = true;
+      continue;
+    }
+    // ---- this step crosses a row boundary
+    float4 tot;
+    if (spread) {  // sum acc over the groups: scan, the total sits in group E-1
+      float4 sc = acc;
+#pragma unroll
+      for (int d = 1; d < E; d <<= 1) {
+        const float4 o = shfl4_up(sc, d * G);
+        if (gi >= d) add4(sc, o);
+      }
+      tot = shfl4(sc, (E - 1) * G + sub);
+    } else {
+      tot = shfl4(acc, carry_g * G + sub);
+    }
+#pragma unroll
+    for (int d = 1; d < E; d <<= 1) {  // segmented scan of v over the groups by key
+      const uint32_t okey = __shfl_up_sync(kFull, key, d * G);
+      const float4 o = shfl4_up(v, d * G);
+      if (gi >= d && okey == key) add4(v, o);
+    }
+    const uint32_t nkey = __shfl_down_sync(kFull, key, G);
+    const unsigned vmask = __ballot_sync(kFull, valid && sub == 0);
+    const int last_g = (31 - __clz(vmask)) / G;
+    const bool seg_end = valid && (gi == E - 1 || nkey != key);
+    const bool is_last = gi == last_g;
+    if (key == cur) add4(v, tot);
+    const uint32_t key0 = __shfl_sync(kFull, key, 0);
+    if (key0 != cur) {  // the open row ended exactly at the previous step
+      float g[RP];
+      group_row<RP>(tot, 0, g);
+      finalize_row_warp_all<RP>(a, bsn, cur, g, lane);
+    }
+    unsigned fin = __ballot_sync(kFull, seg_end && !is_last && sub == 0);
+    while (fin) {
+      const int src = __ffs(fin) - 1;
+      fin &= fin - 1;
+      float g[RP];
+      group_row<RP>(v, src / G, g);
+      finalize_row_warp_all<RP>(a, bsn, __shfl_sync(kFull, key, src), g, lane);
+    }
+    cur = __shfl_sync(kFull, key, last_g * G);
+    if (is_last) {
+      acc = v;
+    } else {
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    spread = false;
+    carry_g = last_g;
+  }
+  // ---- the open row at the chunk end
+  float4 tot;
+  if (spread) {
+    float4 sc = acc;
+#pragma unroll
+    for (int d = 1; d < E; d <<= 1) {
+      const float4 o = shfl4_up(sc, d * G);
+      if (gi >= d) add4(sc, o);
+    }
+    tot = shfl4(sc, (E - 1) * G + sub);
+  } else {
+    tot = shfl4(acc, carry_g * G + sub);
+  }
+  float g[RP];
+  group_row<RP>(tot, 0, g);
+  if (ch.piece < 0) {
+    finalize_row_warp_all<RP>(a, bsn, cur, g, lane);
+  } else if (lane == 0) {
+    double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(g[r]);
+  }
+}
+
 // Rows longer than a chunk: sum their pieces in piece order, then finalise.
 template <int RP>
 __global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
@@ -423,7 +641,10 @@ int factor_launch(Session& s, FactorArgs& a) {
   const int block = 256, wpb = block / 32;
   if (a.n_chunks) {
     const unsigned grid = (a.n_chunks + wpb - 1) / wpb;
-    factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
+    if constexpr (RP >= 16)
+      factor_group_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
+    else
+      factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
     ++s.launches;
   }

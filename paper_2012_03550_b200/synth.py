@@ -38,6 +38,15 @@ class SynthSpec:
     seed: int = 1
     test_fraction: float = 0.1
 
+    @property
+    def order_count(self) -> int:
+        return len(self.dims)
+
+    @property
+    def unit_sigma(self) -> float:
+        """Teacher / init scale giving xhat unit variance: (J R^(1/N))^(-1/4)."""
+        return (self.teacher_j * self.teacher_r ** (1.0 / len(self.dims))) ** -0.25
+
 
 CONFIGS = {
     2: SynthSpec(dims=(480000, 17800, 2200), zipf=(1.1, 1.1, 0.0), nnz=100_000_000, teacher_j=10,
@@ -79,6 +88,28 @@ def _unkey(key, dims):
     return out
 
 
+def _draw_tuples_wide(spec: SynthSpec, device):
+    """Index spaces beyond 2^63 cells (config 4): dedupe whole coordinate
+    tuples; rows come back sorted lexicographically from the last mode, i.e.
+    by linear position with mode 1 fastest."""
+    gen = torch.Generator(device=device)
+    gen.manual_seed(spec.seed)
+    cols = None
+    while True:
+        batch = max(1 << 20, spec.nnz - (0 if cols is None else cols.shape[0]) + spec.nnz // 64)
+        idx = torch.stack([_draw_mode(d, s, batch, gen, device) for d, s in zip(spec.dims, spec.zipf)], 1)
+        cols = idx if cols is None else torch.cat([cols, idx])
+        rev = cols.flip(1)
+        uniq, inv = torch.unique(rev, dim=0, return_inverse=True)
+        first = torch.full((uniq.shape[0],), cols.shape[0], dtype=torch.int64, device=device)
+        first.scatter_reduce_(0, inv, torch.arange(cols.shape[0], device=device), reduce="amin")
+        if uniq.shape[0] >= spec.nnz:
+            keep = torch.sort(first).values[: spec.nnz]  # first occurrences in draw order
+            sel = cols[keep].flip(1)
+            order = torch.unique(sel, dim=0)  # lexicographic = linear position order
+            return [order[:, spec.order_count - 1 - k] for k in range(spec.order_count)]
+
+
 def draw_positions(spec: SynthSpec, device) -> torch.Tensor:
     """Exactly spec.nnz distinct linear keys, first-drawn wins, sorted."""
     gen = torch.Generator(device=device)
@@ -117,9 +148,12 @@ def generate(spec: SynthSpec, device="cuda"):
     """Returns (train, test), each (coords u32 [nnz,N] 1-based, values f64) as
     torch tensors on `device`, plus the mode-sorted permutations of train."""
     device = torch.device(device)
-    keys = draw_positions(spec, device)
-    idx = _unkey(keys, spec.dims)
-    del keys
+    if math.prod(spec.dims) >= 2**62:
+        idx = _draw_tuples_wide(dataclasses.replace(spec), device)
+    else:
+        keys = draw_positions(spec, device)
+        idx = _unkey(keys, spec.dims)
+        del keys
     A, B = teacher(spec, device)
     Q = [a @ b for a, b in zip(A, B)]
     nnz = spec.nnz

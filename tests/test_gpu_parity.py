@@ -158,6 +158,12 @@ CASES = [
     dict(dims=(50, 40, 30), J=(10, 10, 10), R=10, nnz=8000, batch_m=1024),
     dict(dims=(20, 20, 20), J=(16, 12, 16), R=12, nnz=3000, batch_m=300),
     dict(dims=(20, 20, 20), J=(32, 32, 32), R=32, nnz=3000, batch_m=300),
+    dict(dims=(300, 40, 30), J=(16, 16, 16), R=16, nnz=20000, batch_m=500),   # wide-row kernels
+    dict(dims=(300, 40, 30), J=(20, 20, 20), R=20, nnz=20000, batch_m=500),
+    dict(dims=(7, 500, 30), J=(24, 24, 24), R=22, nnz=20000, batch_m=500),
+    dict(dims=(300, 40, 30), J=(28, 28, 28), R=27, nnz=20000, batch_m=500),
+    dict(dims=(9, 8, 7, 6), J=(16, 16, 16, 16), R=16, nnz=3000, batch_m=256),
+    dict(dims=(9, 8, 7, 6, 5), J=(10, 10, 10, 10, 10), R=10, nnz=3000, batch_m=256),
 ]
 
 
