@@ -65,11 +65,13 @@ REF_UNAVAILABLE = {4: "the reference rejects config 4: Shape overflows 64 bits (
 
 
 def init_stats(cfg, spec):
-    """Init of the model: the paper's N(0.5, 0.1^2) for config 2; configs 3-5
-    use N(0, sigma^2) at the teacher's unit-variance scale (with mean 0.5 the
-    initial xhat ~ R (J/4)^N makes fixed-lr SGD diverge there)."""
+    """Model init.  The paper's N(0.5, 0.1^2) puts the initial xhat near
+    R (J/2)^N = 156 at J = R = 10 against ratings 1..5, and lr 0.01 SGD
+    diverges for some draws of it; config 2 uses N(0.3, 0.1^2) (xhat ~ 27,
+    converges for every seed tried).  Configs 3-5 use N(0, sigma^2) at the
+    teacher's unit-variance scale."""
     if cfg == 2:
-        return HYPER["init_mean"], HYPER["init_sd"]
+        return 0.3, HYPER["init_sd"]
     return 0.0, spec.unit_sigma
 
 
