@@ -47,6 +47,7 @@ struct FactorArgs {
   uint32_t n_splits;
   double* piece;   // n_pieces x RP
   double* xport;   // 2 x RP: summed pieces of rows cut by this rank's slice
+  uint64_t qbase;  // row_ptr value of the copy's first record (shard slice start)
   double lr, reg;
   int* flag;
 };
@@ -216,6 +217,57 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
   if (wid >= a.n_chunks) return;
   const Chunk ch = a.chunks[wid];
   const float* Qn = a.P.Q[a.n];
+
+  if (ch.pad) {
+    // A chunk of short rows (< 32 entries each): lane l owns rows r0+l,
+    // r0+l+32, ... -- no cross-lane reduction; every lane finalises its own
+    // rows together in SIMT.
+    const uint32_t r0 = a.keys[ch.begin], r1 = a.keys[ch.end - 1];
+    for (uint32_t row = r0 + lane; row <= r1; row += 32) {
+      const uint32_t b = static_cast<uint32_t>(a.row_ptr[row] - a.qbase);
+      const uint32_t e = static_cast<uint32_t>(a.row_ptr[row + 1] - a.qbase);
+      if (b == e) continue;
+      const float4* qn = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(row) * RP);
+      float4 h[RP / 4];
+#pragma unroll
+      for (int r = 0; r < RP / 4; ++r) h[r] = qn[r];
+      float g[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) g[r] = 0.f;
+      for (uint32_t q = b; q < e; ++q) {
+        const float x = ld_stream(a.val + q);
+        float c[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) c[r] = 1.f;
+#pragma unroll
+        for (int j = 0; j < NO; ++j) {
+          const float4* qk =
+              reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ld_stream(a.oidx[j] + q)) * RP);
+#pragma unroll
+          for (int r = 0; r < RP / 4; ++r) {
+            const float4 t = __ldg(qk + r);
+            c[4 * r] *= t.x;
+            c[4 * r + 1] *= t.y;
+            c[4 * r + 2] *= t.z;
+            c[4 * r + 3] *= t.w;
+          }
+        }
+        float p = 0.f;
+#pragma unroll
+        for (int r = 0; r < RP / 4; ++r) {
+          p = fmaf(h[r].x, c[4 * r], p);
+          p = fmaf(h[r].y, c[4 * r + 1], p);
+          p = fmaf(h[r].z, c[4 * r + 2], p);
+          p = fmaf(h[r].w, c[4 * r + 3], p);
+        }
+        const float t = p - x;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) g[r] = fmaf(t, c[r], g[r]);
+      }
+      finalize_row<RP>(a, bsn, row, g);
+    }
+    return;
+  }
 
   // software pipeline: records of the next window
   uint32_t pk = kNone, pi[NO];
@@ -705,6 +757,7 @@ FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h, bool subse
   a.n_splits = subset ? rs.n_splits : mp.n_splits;
   a.piece = s.piece_partials;
   a.xport = s.export_buf;
+  a.qbase = subset ? 0 : mp.shard.qb;
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;

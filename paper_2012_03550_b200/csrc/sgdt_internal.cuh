@@ -27,6 +27,7 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 // Factor-phase work unit: entries [begin, end) of the mode-sorted copy.
 // piece < 0: the chunk holds whole rows; otherwise it is piece `piece` of a
 // row longer than the chunk size (finalised by the split-row kernel).
+// pad = 1: whole rows that are all short -- one row per lane.
 struct Chunk {
   uint32_t begin;
   uint32_t end;

@@ -148,6 +148,9 @@ void host_mode_layout(const sgdt_tensor_desc* d, int n, std::vector<uint64_t>& o
   for (uint64_t e = 0; e < d->nnz; ++e) perm[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
 }
 
+// Rows shorter than this are processed one row per lane (Chunk::pad = 1).
+constexpr uint64_t kShortRow = 32;
+
 // nnz-balanced chunk schedule over the mode-sorted entries [qb, qe) (the
 // whole order for a single-GPU session; this rank's partition_even slice for a
 // sharded one): whole rows packed greedily up to chunk_size, longer rows cut
@@ -199,11 +202,12 @@ void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, ui
     }
     if (open && (e - cur.begin) > chunk_size) close();
     if (!open) {
-      cur = Chunk{static_cast<uint32_t>(b), static_cast<uint32_t>(e), -1, 0};
+      cur = Chunk{static_cast<uint32_t>(b), static_cast<uint32_t>(e), -1, 1};
       open = true;
     } else {
       cur.end = static_cast<uint32_t>(e);
     }
+    if (cnt >= kShortRow) cur.pad = 0;  // pad = 1: every row of the chunk is short
   }
   close();
 }
