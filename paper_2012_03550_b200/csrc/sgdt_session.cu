@@ -148,8 +148,9 @@ void host_mode_layout(const sgdt_tensor_desc* d, int n, std::vector<uint64_t>& o
   for (uint64_t e = 0; e < d->nnz; ++e) perm[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
 }
 
-// Rows shorter than this are processed one row per lane (Chunk::pad = 1).
-constexpr uint64_t kShortRow = 32;
+// Rows shorter than this are processed one row per lane / lane group
+// (Chunk::pad = 1); 64 measured best on config 2 (16: +9%, 256: +5%).
+constexpr uint64_t kShortRow = 64;
 
 // nnz-balanced chunk schedule over the mode-sorted entries [qb, qe) (the
 // whole order for a single-GPU session; this rank's partition_even slice for a
