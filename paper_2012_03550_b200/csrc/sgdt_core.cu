@@ -49,12 +49,6 @@ struct CoreArgs {
   uint32_t cap;       // samples per CTA slice (upper bound)
 };
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 template <int RP>
 __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -94,11 +88,14 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
     lxh = lc + static_cast<uint64_t>(a.cap) * RP;
     lx = lxh + a.cap;
   } else {
-    la = a.sa + s0 * a.js;
-    lc = a.sc + s0 * RP;
-    lxh = a.sxh + s0;
-    lx = a.sx + s0;
+    const uint64_t cb = static_cast<uint64_t>(blockIdx.x) * a.cap;
+    la = a.sa + cb * a.js;
+    lc = a.sc + cb * RP;
+    lxh = a.sxh + cb;
+    lx = a.sx + cb;
   }
+  // per-sample vectors are stored transposed (la[j*cap + ls], lc[r*cap + ls])
+  // so that thread-per-sample passes are coalesced / bank-conflict free
   uint32_t step = 0;
 
   for (int n = 0; n < a.P.order; ++n) {
@@ -132,7 +129,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
       for (int r = 0; r < RP; ++r) p[r] = 0.f;
       for (uint32_t j = 0; j < jn; ++j) {
         const float av = arow[j];
-        la[ls * a.js + j] = av;
+        la[j * a.cap + ls] = av;
 #pragma unroll
         for (int r = 0; r < RP; ++r) p[r] = fmaf(av, bs[n][j * RP + r], p[r]);
       }
@@ -140,7 +137,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
         xh = fmaf(c[r], p[r], xh);
-        lc[ls * RP + r] = c[r];
+        lc[r * a.cap + ls] = c[r];
       }
       lxh[ls] = xh;
       lx[ls] = a.rec_val[e];
@@ -151,15 +148,25 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
       // ---- partial V over this CTA's slice: V_j = sum_s c_{s,rc} (xhat_s - x_s) a_{s,j}
       double* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
       {
-        // thread-per-sample terms, warp reduction per j (fixed order)
-        for (uint32_t j = 0; j < jn; ++j) {
-          float v = 0.f;
+        // thread-per-sample terms, 8 columns of a per pass, then one warp
+        // reduction per j (fixed order)
+        for (uint32_t j0 = 0; j0 < jn; j0 += 8) {
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = 0.f;
           for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
-            const float t = lc[ls * RP + rc] * (lxh[ls] - lx[ls]);
-            v = fmaf(t, la[ls * a.js + j], v);
+            const float t = lc[rc * a.cap + ls] * (lxh[ls] - lx[ls]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (j0 + q < jn) v[q] = fmaf(t, la[(j0 + q) * a.cap + ls], v[q]);
           }
-          v = warp_sum(v);
-          if (lane == 0) wpart[warp * a.js + j] = static_cast<double>(v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float w = v[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            if (lane == 0 && j0 + q < jn) wpart[warp * a.js + j0 + q] = static_cast<double>(w);
+          }
         }
         __syncthreads();
         if (tid < static_cast<int>(jn)) {
@@ -195,8 +202,8 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
       if (rc + 1 < a.P.R) {
         for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
           float d = 0.f;
-          for (uint32_t j = 0; j < jn; ++j) d = fmaf(la[ls * a.js + j], dbv[j], d);
-          lxh[ls] = fmaf(lc[ls * RP + rc], d, lxh[ls]);
+          for (uint32_t j = 0; j < jn; ++j) d = fmaf(la[j * a.cap + ls], dbv[j], d);
+          lxh[ls] = fmaf(lc[rc * a.cap + ls], d, lxh[ls]);
         }
         __syncthreads();
       }

@@ -341,10 +341,11 @@ int ensure_core_capacity(Session& s, uint64_t m) {
   F(s.cs_part);
   uint32_t js = 0;
   for (int k = 0; k < s.order; ++k) js = std::max(js, s.J[k]);
-  TRY(dalloc(&s.cs_a, m * js));
-  TRY(dalloc(&s.cs_c, m * s.RP));
-  TRY(dalloc(&s.cs_xhat, m));
-  TRY(dalloc(&s.cs_x, m));
+  const uint64_t mm = m + s.num_sms;  // per-CTA slices of ceil(m / grid) samples
+  TRY(dalloc(&s.cs_a, mm * js));
+  TRY(dalloc(&s.cs_c, mm * s.RP));
+  TRY(dalloc(&s.cs_xhat, mm));
+  TRY(dalloc(&s.cs_x, mm));
   TRY(dalloc(&s.cs_part, 2ull * s.num_sms * js));
   s.cs_cap = m;
   return SGDT_OK;
