@@ -49,28 +49,157 @@ struct CoreArgs {
   uint32_t cap;       // samples per CTA slice (upper bound)
 };
 
+// Warp transpose-reduce: afterwards lane l holds the warp-wide sum of v[l]
+// (31 shuffles for 32 values; fixed order, so every run forms the same sums).
+__device__ __forceinline__ float warp_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
+// One pass over the CTA's samples for columns j0..j0+31 of V_rcn:
+//   (upd >= 0)  xhat_s += c_{s,upd} (a_s . delta_b)    -- column upd was just stepped
+//   v_j += c_{s,rcn} (xhat_s - x_s) a_{s,j}
+// a_s is loaded once into registers and feeds both terms.
+__device__ __forceinline__ void column_pass(const float* la, const float* lc, float* lxh, const float* lx,
+                                            const float* dbv, uint32_t cap, uint32_t nloc, uint32_t jn,
+                                            int upd, uint32_t rcn, uint32_t j0, float (&v)[32]) {
+  for (uint32_t ls = threadIdx.x; ls < nloc; ls += blockDim.x) {
+    float av[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * cap + ls] : 0.f;
+    float xh = lxh[ls];
+    if (upd >= 0) {
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) d = fmaf(av[q], dbv[q], d);
+      for (uint32_t j = 32; j < jn; ++j) d = fmaf(la[j * cap + ls], dbv[j], d);
+      xh = fmaf(lc[upd * cap + ls], d, xh);
+      lxh[ls] = xh;
+    }
+    const float t = lc[rcn * cap + ls] * (xh - lx[ls]);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = fmaf(t, av[q], v[q]);
+  }
+}
+
+// Q^(k) rows = A^(k) rows x B^(k), a warp per tile of 32 rows: the tile of A
+// (contiguous, row stride J) is staged through a per-warp shared buffer so
+// both the A reads and the Q writes are coalesced; lane l then forms row
+// i0 + l in registers (j ascending, the same fmaf order as a per-row loop).
+constexpr int kQStage = 32 * 33;  // floats per warp
+
 template <int RP>
-__global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
+__device__ __forceinline__ void q_rows_tiled(const float* __restrict__ A, float* __restrict__ Q, uint32_t J,
+                                             const float* bsk, uint64_t nrows, uint64_t gw, uint64_t nw,
+                                             float* stage, int lane) {
+  for (uint64_t t = gw; t * 32 < nrows; t += nw) {
+    const uint64_t i0 = t * 32;
+    const uint32_t rows = nrows - i0 < 32 ? static_cast<uint32_t>(nrows - i0) : 32u;
+    float q[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) q[r] = 0.f;
+    for (uint32_t j0 = 0; j0 < J; j0 += 32) {
+      const uint32_t jc = J - j0 < 32 ? J - j0 : 32u;
+      __syncwarp();
+      if (jc == J && rows == 32 && (J & 3) == 0) {
+        // full tile, J <= 32: 8 J float4 loads in flight per warp, then scatter
+        const float4* src4 = reinterpret_cast<const float4*>(A + i0 * J);
+        const uint32_t n4 = 8 * J;
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = u * 32 + lane;
+          v[u] = x < n4 ? __ldg(src4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = u * 32 + lane;
+          if (x < n4) {
+            const uint32_t g = x * 4, row = g / J;
+            float* d = stage + row * 33 + (g - row * J);
+            d[0] = v[u].x;
+            d[1] = v[u].y;
+            d[2] = v[u].z;
+            d[3] = v[u].w;
+          }
+        }
+      } else if (jc == J) {
+        const float* src = A + i0 * J;  // the whole tile is contiguous
+        for (uint32_t g = lane; g < rows * jc; g += 32) {
+          const uint32_t row = g / jc;
+          stage[row * 33 + (g - row * jc)] = __ldg(src + g);
+        }
+      } else {
+        for (uint32_t g = lane; g < rows * jc; g += 32) {
+          const uint32_t row = g / jc, col = g - row * jc;
+          stage[row * 33 + col] = __ldg(A + (i0 + row) * J + j0 + col);
+        }
+      }
+      __syncwarp();
+      if (static_cast<uint32_t>(lane) < rows)
+        for (uint32_t c = 0; c < jc; ++c) {
+          const float av = stage[lane * 33 + c];
+          const float4* br = reinterpret_cast<const float4*>(bsk + (j0 + c) * RP);  // RP % 4 == 0
+#pragma unroll
+          for (int r = 0; r < RP; r += 4) {
+            const float4 b = br[r / 4];
+            q[r] = fmaf(av, b.x, q[r]);
+            q[r + 1] = fmaf(av, b.y, q[r + 1]);
+            q[r + 2] = fmaf(av, b.z, q[r + 2]);
+            q[r + 3] = fmaf(av, b.w, q[r + 3]);
+          }
+        }
+    }
+    __syncwarp();
+    if (static_cast<uint32_t>(lane) < rows) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) stage[lane * (RP + 1) + r] = q[r];
+    }
+    __syncwarp();
+    float* dst = Q + i0 * RP;
+    for (uint32_t g = lane; g < rows * RP; g += 32) {
+      const uint32_t row = g / RP;
+      dst[g] = stage[row * (RP + 1) + (g - row * RP)];
+    }
+  }
+}
+
+constexpr int kCoreBlock = 512;
+
+template <int RP>
+__global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned char smem_raw[];
   // Bs[k]: J_k x RP (zero padded), then per-warp partials, then delta b.
   float* bs_base = reinterpret_cast<float*>(smem_raw);
-  float* bs[kMaxOrder];
+  // offsets (not pointers) so that every access stays a shared-space access
+  uint32_t bso[kMaxOrder];
   uint32_t off = 0;
   for (int k = 0; k < a.P.order; ++k) {
-    bs[k] = bs_base + off;
+    bso[k] = off;
     off += a.P.J[k] * RP;
   }
   const int nwarps = blockDim.x >> 5;
   double* wpart = reinterpret_cast<double*>(bs_base + ((off + 1) & ~1u));  // nwarps x js
-  float* dbv = reinterpret_cast<float*>(wpart + nwarps * a.js);           // js
+  float* dbv = reinterpret_cast<float*>(wpart + nwarps * a.js);           // max(js, 32)
+  const uint32_t dbn = a.js > 32 ? a.js : 32;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int k = 0; k < a.P.order; ++k)
     for (uint32_t i = tid; i < a.P.J[k] * RP; i += blockDim.x) {
       const uint32_t j = i / RP, r = i % RP;
-      bs[k][i] = r < a.P.R ? a.P.B[k][j * a.P.R + r] : 0.f;
+      bs_base[bso[k] + i] = r < a.P.R ? a.P.B[k][j * a.P.R + r] : 0.f;
     }
+  for (uint32_t j = tid; j < dbn; j += blockDim.x) dbv[j] = 0.f;
   __syncthreads();
 
   // this CTA's slice of Psi
@@ -83,7 +212,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
   // when it fits, else the global scratch
   float *la, *lc, *lxh, *lx;
   if (a.local) {
-    la = dbv + a.js;
+    la = dbv + dbn;
     lc = la + static_cast<uint64_t>(a.cap) * a.js;
     lxh = lc + static_cast<uint64_t>(a.cap) * RP;
     lx = lxh + a.cap;
@@ -101,6 +230,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
   for (int n = 0; n < a.P.order; ++n) {
     const uint32_t* batch = a.batch + (a.per_mode ? static_cast<uint64_t>(n) * a.m : 0);
     const uint32_t jn = a.P.J[n];
+    for (uint32_t j = tid; j < dbn; j += blockDim.x) dbv[j] = 0.f;
     // ---- per-sample caches: c_{s,r}, a_s, xhat_s, x_s  (:158-180)
     for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
       const uint32_t e = batch[s0 + ls];
@@ -117,7 +247,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
         for (uint32_t j = 0; j < a.P.J[k]; ++j) {
           const float av = arow[j];
 #pragma unroll
-          for (int r = 0; r < RP; ++r) d[r] = fmaf(av, bs[k][j * RP + r], d[r]);
+          for (int r = 0; r < RP; ++r) d[r] = fmaf(av, bs_base[bso[k] + j * RP + r], d[r]);
         }
 #pragma unroll
         for (int r = 0; r < RP; ++r) c[r] *= d[r];
@@ -131,7 +261,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
         const float av = arow[j];
         la[j * a.cap + ls] = av;
 #pragma unroll
-        for (int r = 0; r < RP; ++r) p[r] = fmaf(av, bs[n][j * RP + r], p[r]);
+        for (int r = 0; r < RP; ++r) p[r] = fmaf(av, bs_base[bso[n] + j * RP + r], p[r]);
       }
       float xh = 0.f;
 #pragma unroll
@@ -144,36 +274,24 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
     }
     __syncthreads();
 
+    int upd = -1;  // column whose step is still to be folded into xhat
     for (uint32_t rc = 0; rc < a.P.R; ++rc, ++step) {
-      // ---- partial V over this CTA's slice: V_j = sum_s c_{s,rc} (xhat_s - x_s) a_{s,j}
+      // ---- partial V over this CTA's slice: V_j = sum_s c_{s,rc} (xhat_s - x_s) a_{s,j},
+      // fused with the xhat refresh for the previous column's step
       double* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
-      {
-        // thread-per-sample terms, 8 columns of a per pass, then one warp
-        // reduction per j (fixed order)
-        for (uint32_t j0 = 0; j0 < jn; j0 += 8) {
-          float v[8];
+      for (uint32_t j0 = 0; j0 < jn; j0 += 32) {
+        float v[32];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = 0.f;
-          for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
-            const float t = lc[rc * a.cap + ls] * (lxh[ls] - lx[ls]);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (j0 + q < jn) v[q] = fmaf(t, la[(j0 + q) * a.cap + ls], v[q]);
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float w = v[q];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-            if (lane == 0 && j0 + q < jn) wpart[warp * a.js + j0 + q] = static_cast<double>(w);
-          }
-        }
-        __syncthreads();
-        if (tid < static_cast<int>(jn)) {
-          double acc = 0.0;
-          for (int w = 0; w < nwarps; ++w) acc += wpart[w * a.js + tid];
-          part[static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x] = acc;  // [j][cta]
-        }
+        for (int q = 0; q < 32; ++q) v[q] = 0.f;
+        column_pass(la, lc, lxh, lx, dbv, a.cap, nloc, jn, j0 == 0 ? upd : -1, rc, j0, v);
+        const float w = warp_reduce32(v, lane);
+        if (j0 + lane < jn) wpart[warp * a.js + j0 + lane] = static_cast<double>(w);
+      }
+      __syncthreads();
+      if (tid < static_cast<int>(jn)) {
+        double acc = 0.0;
+        for (int w = 0; w < nwarps; ++w) acc += wpart[w * a.js + tid];
+        part[static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x] = acc;  // [j][cta]
       }
       grid.sync();
       // ---- every CTA: V_j over the CTA partials (a warp per j, fixed lane
@@ -186,7 +304,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) V += __shfl_xor_sync(0xffffffffu, V, o);
         if (lane == 0) {
-          const float bold = bs[n][j * RP + rc];
+          const float bold = bs_base[bso[n] + j * RP + rc];
           double w = static_cast<double>(bold);
           int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
           w -= a.lr * (V * inv_m + a.reg * w);
@@ -194,19 +312,11 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
           bad |= !isfinite(bnew) ? 4 : 0;
           if (bad && blockIdx.x == 0) atomicOr(a.flag, bad);
           dbv[j] = bnew - bold;
-          bs[n][j * RP + rc] = bnew;
+          bs_base[bso[n] + j * RP + rc] = bnew;
         }
       }
       __syncthreads();
-      // ---- keep xhat current for the next column
-      if (rc + 1 < a.P.R) {
-        for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
-          float d = 0.f;
-          for (uint32_t j = 0; j < jn; ++j) d = fmaf(la[j * a.cap + ls], dbv[j], d);
-          lxh[ls] = fmaf(lc[rc * a.cap + ls], d, lxh[ls]);
-        }
-        __syncthreads();
-      }
+      upd = static_cast<int>(rc);
     }
   }
 
@@ -214,32 +324,19 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs a) {
   if (blockIdx.x == 0)
     for (int k = 0; k < a.P.order; ++k)
       for (uint32_t i = tid; i < a.P.J[k] * a.P.R; i += blockDim.x)
-        a.P.B[k][i] = bs[k][(i / a.P.R) * RP + (i % a.P.R)];
+        a.P.B[k][i] = bs_base[bso[k] + (i / a.P.R) * RP + (i % a.P.R)];
   if (!a.q_refresh) return;
-  for (int k = 0; k < a.P.order; ++k) {
-    const uint32_t jk = a.P.J[k];
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + tid; i < a.P.dims[k];
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-      const float* arow = a.P.A[k] + i * jk;
-      float q[RP];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) q[r] = 0.f;
-      for (uint32_t j = 0; j < jk; ++j) {
-        const float av = arow[j];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) q[r] = fmaf(av, bs[k][j * RP + r], q[r]);
-      }
-      float4* dst = reinterpret_cast<float4*>(a.P.Q[k] + i * RP);
-#pragma unroll
-      for (int r = 0; r < RP; r += 4) dst[r / 4] = make_float4(q[r], q[r + 1], q[r + 2], q[r + 3]);
-    }
-  }
+  float* stage = dbv + dbn + warp * kQStage;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * nwarps;
+  for (int k = 0; k < a.P.order; ++k)
+    q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs_base + bso[k], a.P.dims[k], gw, nw, stage, lane);
 }
 
 // Standalone Q refresh (used after set_model and by the factor phase when the
 // core phase is frozen).
 template <int RP>
-__global__ void q_refresh_kernel(Params P, int k) {
+__global__ void __launch_bounds__(256) q_refresh_kernel(Params P, int k) {
   extern __shared__ float bsk[];
   const uint32_t jk = P.J[k];
   for (uint32_t i = threadIdx.x; i < jk * RP; i += blockDim.x) {
@@ -247,30 +344,20 @@ __global__ void q_refresh_kernel(Params P, int k) {
     bsk[i] = r < P.R ? P.B[k][j * P.R + r] : 0.f;
   }
   __syncthreads();
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < P.dims[k];
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const float* arow = P.A[k] + i * jk;
-    float q[RP];
-#pragma unroll
-    for (int r = 0; r < RP; ++r) q[r] = 0.f;
-    for (uint32_t j = 0; j < jk; ++j) {
-      const float av = arow[j];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) q[r] = fmaf(av, bsk[j * RP + r], q[r]);
-    }
-    float4* dst = reinterpret_cast<float4*>(P.Q[k] + i * RP);
-#pragma unroll
-    for (int r = 0; r < RP; r += 4) dst[r / 4] = make_float4(q[r], q[r + 1], q[r + 2], q[r + 3]);
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* stage = bsk + jk * RP + warp * kQStage;
+  q_rows_tiled<RP>(P.A[k], P.Q[k], jk, bsk, P.dims[k],
+                   static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + warp,
+                   static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5), stage, lane);
 }
 
 template <int RP>
 int core_launch_rp(Session& s, CoreArgs& a) {
-  const int block = 256;
+  const int block = kCoreBlock;
   size_t bs_floats = 0;
   for (int k = 0; k < s.order; ++k) bs_floats += s.J[k] * RP;
   size_t smem = ((bs_floats + 1) & ~size_t(1)) * sizeof(float) + (block / 32) * a.js * sizeof(double) +
-                a.js * sizeof(float);
+                (a.js > 32 ? a.js : 32) * sizeof(float);
   auto kern = core_kernel<RP>;
   // one CTA per SM keeps grid.sync cheap; small batches use fewer CTAs
   uint64_t want = (a.m + 127) / 128;
@@ -283,8 +370,10 @@ int core_launch_rp(Session& s, CoreArgs& a) {
   }
   a.cap = static_cast<uint32_t>((a.m + grid - 1) / grid);
   const size_t local = static_cast<size_t>(a.cap) * (a.js + RP + 2) * sizeof(float);
-  a.local = smem + local <= 200 * 1024;
-  if (a.local) smem += local;
+  const size_t stage = static_cast<size_t>(block / 32) * kQStage * sizeof(float);  // tail Q refresh
+  const size_t tail_local = local > stage ? local : stage;
+  a.local = smem + tail_local <= 200 * 1024;
+  smem += a.local ? tail_local : stage;
   if (smem > 48 * 1024)
     SGDT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
@@ -300,7 +389,10 @@ int core_launch_rp(Session& s, CoreArgs& a) {
 
 template <int RP>
 int q_launch_rp(Session& s, int k) {
-  const size_t smem = s.J[k] * RP * sizeof(float);
+  const size_t smem = (s.J[k] * RP + 8 * kQStage) * sizeof(float);
+  if (smem > 48 * 1024)
+    SGDT_CUDA(cudaFuncSetAttribute(q_refresh_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
   uint64_t blocks = (s.dims[k] + 255) / 256;
   if (blocks > static_cast<uint64_t>(s.num_sms) * 8) blocks = s.num_sms * 8;
   q_refresh_kernel<RP><<<static_cast<unsigned>(blocks), 256, smem, s.stream>>>(s.P, k);
