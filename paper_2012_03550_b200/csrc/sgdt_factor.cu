@@ -65,12 +65,22 @@ __device__ __forceinline__ float ld_stream(const float* p) {
   return v;
 }
 
+// B^(n) lives in shared memory with row stride RP + 1 (odd), so the
+// lane-per-j pass (F_j = B[j,:] . g) and the lane-per-r pass (q_r = a . B[:,r])
+// both read it without bank conflicts.  Rows are zero padded up to a multiple
+// of 4 so vectorised broadcasts may run past J.
+template <int RP>
+__host__ __device__ constexpr int bstride() {
+  return RP <= 12 ? RP : RP + 1;
+}
+constexpr int kWarpScratch = 96;  // floats per warp: a row (<= 64) + g (<= 32)
+
 template <int RP>
 __device__ __forceinline__ void load_bsn(const FactorArgs& a, float* bsn) {
-  const uint32_t jn = a.P.J[a.n];
-  for (uint32_t i = threadIdx.x; i < jn * RP; i += blockDim.x) {
-    const uint32_t j = i / RP, r = i % RP;
-    bsn[i] = r < a.P.R ? a.P.B[a.n][j * a.P.R + r] : 0.f;
+  const uint32_t jn = a.P.J[a.n], j4 = (jn + 3) & ~3u;
+  for (uint32_t i = threadIdx.x; i < j4 * bstride<RP>(); i += blockDim.x) {
+    const uint32_t j = i / bstride<RP>(), r = i % bstride<RP>();
+    bsn[i] = j < jn && r < a.P.R ? a.P.B[a.n][j * a.P.R + r] : 0.f;
   }
 }
 
@@ -80,7 +90,7 @@ struct RowUpdate {
   float* A;                 // A^(n)
   float* Q;                 // Q^(n)
   const uint32_t* row_ptr;  // mode-n row offsets
-  const float* bsn;         // B^(n) in shared memory, J x RP
+  const float* bsn;         // B^(n) in shared memory, J x bstride
   uint32_t jn;
   float lr, reg;
   int* flag;
@@ -101,7 +111,7 @@ __device__ __noinline__ void finalize_row_impl(RowUpdate u, uint32_t row, const 
   for (uint32_t j = 0; j < u.jn; ++j) {
     float F = 0.f;
 #pragma unroll
-    for (int r = 0; r < RP; ++r) F = fmaf(u.bsn[j * RP + r], gr[r], F);
+    for (int r = 0; r < RP; ++r) F = fmaf(u.bsn[j * bstride<RP>() + r], gr[r], F);
     const float w = arow[j];
     bad |= !isfinite(w) || !isfinite(F);
     const float wn = w - u.lr * fmaf(F, inv, u.reg * w);
@@ -114,7 +124,7 @@ __device__ __noinline__ void finalize_row_impl(RowUpdate u, uint32_t row, const 
     float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t j = 0; j < u.jn; ++j) {
       const float wf = arow[j];
-      const float* b = u.bsn + j * RP + 4 * s;
+      const float* b = u.bsn + j * bstride<RP>() + 4 * s;
       q.x = fmaf(wf, b[0], q.x);
       q.y = fmaf(wf, b[1], q.y);
       q.z = fmaf(wf, b[2], q.z);
@@ -139,12 +149,12 @@ __device__ __forceinline__ void finalize_row(const FactorArgs& a, const float* b
   finalize_row_impl<RP>(row_update(a, bsn), row, gf);
 }
 
-// The same row update done by the whole warp: g (held by lane `src`) is
-// broadcast, lane j updates a_j, lane r rebuilds Q^(n)[row][r].  ~RP + J
-// shuffles instead of ~J*RP serial FMAs on one lane.
+// The same row update done by the whole warp: lane j updates a_j, the new row
+// goes through the warp's shared scratch (one store, broadcast reads) and lane
+// r rebuilds Q^(n)[row][r].  All shared reads are conflict-free or broadcast.
 template <int RP>
 __device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const float* bsn, uint32_t row,
-                                                      const float (&gg)[RP], uint32_t lane) {
+                                                      const float (&gg)[RP], uint32_t lane, float* wsc) {
   const uint32_t jn = a.P.J[a.n];
   const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
   const float inv = 1.0f / static_cast<float>(cnt);
@@ -158,32 +168,53 @@ __device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const
     if (j < jn) {
       float F = 0.f;
 #pragma unroll
-      for (int r = 0; r < RP; ++r) F = fmaf(bsn[j * RP + r], gg[r], F);
+      for (int r = 0; r < RP; ++r) F = fmaf(bsn[j * bstride<RP>() + r], gg[r], F);
       const float w = arow[j];
       wn = w - lr * fmaf(F, inv, reg * w);
       bad |= !isfinite(w) || !isfinite(F) || !isfinite(wn);
       arow[j] = wn;
     }
-    const uint32_t jend = jn - j0 < 32 ? jn - j0 : 32;
-    for (uint32_t t = 0; t < jend; ++t) {
-      const float aj = __shfl_sync(0xffffffffu, wn, t);
-      if (lane < RP) q = fmaf(aj, bsn[(j0 + t) * RP + lane], q);
+    if constexpr (RP <= 12) {  // narrow rows: J shuffles are cheaper than the scratch round trip
+      const uint32_t jend = jn - j0 < 32 ? jn - j0 : 32;
+      for (uint32_t t = 0; t < jend; ++t) {
+        const float aj = __shfl_sync(0xffffffffu, wn, t);
+        if (lane < RP) q = fmaf(aj, bsn[(j0 + t) * bstride<RP>() + lane], q);
+      }
+    } else {
+      wsc[j] = wn;  // zero past jn
     }
   }
-  if (lane < RP) a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+  if constexpr (RP <= 12) {
+    if (lane < RP) a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
+    return;
+  }
+  __syncwarp();
+  if (lane < RP) {
+    const float4* a4 = reinterpret_cast<const float4*>(wsc);
+    for (uint32_t t = 0; t < jn; t += 4) {
+      const float4 w4 = a4[t / 4];
+      const float* b = bsn + t * bstride<RP>() + lane;
+      q = fmaf(w4.x, b[0], q);
+      q = fmaf(w4.y, b[bstride<RP>()], q);
+      q = fmaf(w4.z, b[2 * bstride<RP>()], q);
+      q = fmaf(w4.w, b[3 * bstride<RP>()], q);
+    }
+    a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+  }
+  __syncwarp();
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
 }
 
-// The same row update done by the whole warp: g (held by lane `src`) is
-// broadcast, lane j updates a_j, lane r rebuilds Q^(n)[row][r].  ~RP + J
-// shuffles instead of ~J*RP serial FMAs on one lane.
+// g held by lane `src` (one-entry-per-lane kernel): broadcast, then the warp
+// row update.
 template <int RP>
 __device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const float* bsn, uint32_t row,
-                                                  const float (&g)[RP], int src, uint32_t lane) {
+                                                  const float (&g)[RP], int src, uint32_t lane, float* wsc) {
   float gg[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) gg[r] = __shfl_sync(0xffffffffu, g[r], src);
-  finalize_row_warp_all<RP>(a, bsn, row, gg, lane);
+  finalize_row_warp_all<RP>(a, bsn, row, gg, lane, wsc);
 }
 
 template <int RP, typename T>
@@ -209,10 +240,12 @@ constexpr int factor_min_blocks() {
 // to fp64 at every row boundary.
 template <int RP, int NO>
 __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
-  __shared__ float bsn[SGDT_MAX_J * RP];
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
+  __shared__ __align__(16) float wscr[8 * kWarpScratch];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
+  float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
   const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= a.n_chunks) return;
   const Chunk ch = a.chunks[wid];
@@ -363,7 +396,7 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
 #pragma unroll
       for (int r = 0; r < RP; ++r) tot[r] = acc[r] + (static_cast<int>(lane) < b ? v[r] : 0.f);
       warp_allreduce<RP>(tot);
-      finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);
+      finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane, wsc);
       cur = __shfl_sync(kFull, key, b);
 #pragma unroll
       for (int r = 0; r < RP; ++r) acc[r] = static_cast<int>(lane) >= b ? v[r] : 0.f;
@@ -400,12 +433,12 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
     }
     const uint32_t key0 = __shfl_sync(kFull, key, 0);
     unsigned fin = __ballot_sync(kFull, seg_end && !is_last);
-    if (key0 != cur) finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);  // row ended at the window edge
+    if (key0 != cur) finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane, wsc);  // row ended at the window edge
     if (__popc(fin) <= 4) {
       while (fin) {
         const int src = __ffs(fin) - 1;
         fin &= fin - 1;
-        finalize_row_warp<RP>(a, bsn, __shfl_sync(kFull, key, src), v, src, lane);
+        finalize_row_warp<RP>(a, bsn, __shfl_sync(kFull, key, src), v, src, lane, wsc);
       }
     } else if (seg_end && !is_last) {
       finalize_row<RP>(a, bsn, key, v);
@@ -427,7 +460,7 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
     for (int r = 0; r < RP; ++r) tot[r] = __shfl_sync(kFull, tot[r], carry_lane);
   }
   if (ch.piece < 0) {
-    finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane);
+    finalize_row_warp<RP>(a, bsn, cur, tot, 0, lane, wsc);
   } else if (lane == 0) {
     double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
 #pragma unroll
@@ -480,26 +513,33 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
   a.w += b.w;
 }
 
-// All lanes receive the RP components held by group `grp` (4 per lane).
+// All lanes receive the RP components held by group `grp` (4 per lane): one
+// float4 store per group lane into the warp's scratch, then broadcast reads.
 template <int RP>
-__device__ __forceinline__ void group_row(const float4& v, int grp, float (&g)[RP]) {
+__device__ __forceinline__ void group_row(const float4& v, int grp, float (&g)[RP], int gi, int sub, float* gsc) {
+  if (gi == grp) reinterpret_cast<float4*>(gsc)[sub] = v;
+  __syncwarp();
 #pragma unroll
   for (int s = 0; s < RP / 4; ++s) {
-    const float4 o = shfl4(v, grp * (RP / 4) + s);
+    const float4 o = reinterpret_cast<const float4*>(gsc)[s];
     g[4 * s] = o.x;
     g[4 * s + 1] = o.y;
     g[4 * s + 2] = o.z;
     g[4 * s + 3] = o.w;
   }
+  __syncwarp();
 }
 
 template <int RP, int NO>
 __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
   constexpr int G = Lanes<RP>::G, E = Lanes<RP>::E;
-  __shared__ float bsn[SGDT_MAX_J * RP];
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
+  __shared__ __align__(16) float wscr[8 * kWarpScratch];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
+  float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
+  float* gsc = wsc + 64;
   const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= a.n_chunks) return;
   const Chunk ch = a.chunks[wid];
@@ -600,16 +640,16 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
     const uint32_t key0 = __shfl_sync(kFull, key, 0);
     if (key0 != cur) {  // the open row ended exactly at the previous step
       float g[RP];
-      group_row<RP>(tot, 0, g);
-      finalize_row_warp_all<RP>(a, bsn, cur, g, lane);
+      group_row<RP>(tot, 0, g, gi, sub, gsc);
+      finalize_row_warp_all<RP>(a, bsn, cur, g, lane, wsc);
     }
     unsigned fin = __ballot_sync(kFull, seg_end && !is_last && sub == 0);
     while (fin) {
       const int src = __ffs(fin) - 1;
       fin &= fin - 1;
       float g[RP];
-      group_row<RP>(v, src / G, g);
-      finalize_row_warp_all<RP>(a, bsn, __shfl_sync(kFull, key, src), g, lane);
+      group_row<RP>(v, src / G, g, gi, sub, gsc);
+      finalize_row_warp_all<RP>(a, bsn, __shfl_sync(kFull, key, src), g, lane, wsc);
     }
     cur = __shfl_sync(kFull, key, last_g * G);
     if (is_last) {
@@ -634,9 +674,9 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
     tot = shfl4(acc, carry_g * G + sub);
   }
   float g[RP];
-  group_row<RP>(tot, 0, g);
+  group_row<RP>(tot, 0, g, gi, sub, gsc);
   if (ch.piece < 0) {
-    finalize_row_warp_all<RP>(a, bsn, cur, g, lane);
+    finalize_row_warp_all<RP>(a, bsn, cur, g, lane, wsc);
   } else if (lane == 0) {
     double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
 #pragma unroll
@@ -647,7 +687,7 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
 // Rows longer than a chunk: sum their pieces in piece order, then finalise.
 template <int RP>
 __global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
-  __shared__ float bsn[SGDT_MAX_J * RP];
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
@@ -677,7 +717,7 @@ __global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
 template <int RP>
 __global__ void __launch_bounds__(256) factor_finish_kernel(FactorArgs a, uint32_t k, const uint32_t* rows,
                                                             const double* gm) {
-  __shared__ float bsn[SGDT_MAX_J * RP];
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
