@@ -149,12 +149,13 @@ __device__ __forceinline__ void finalize_row(const FactorArgs& a, const float* b
   finalize_row_impl<RP>(row_update(a, bsn), row, gf);
 }
 
-// The same row update done by the whole warp: lane j updates a_j, the new row
-// goes through the warp's shared scratch (one store, broadcast reads) and lane
-// r rebuilds Q^(n)[row][r].  All shared reads are conflict-free or broadcast.
-template <int RP>
-__device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const float* bsn, uint32_t row,
-                                                      const float (&gg)[RP], uint32_t lane, float* wsc) {
+// The same row update done by the whole warp, g (RP floats) in the warp's
+// shared scratch: lane j updates a_j, the new row goes through the scratch
+// (one store, broadcast reads) and lane r rebuilds Q^(n)[row][r].  All shared
+// reads are conflict-free or broadcast.
+template <int RP, typename GetG>
+__device__ __forceinline__ void finalize_row_warp_core(const FactorArgs& a, const float* bsn, uint32_t row,
+                                                       GetG get_g, uint32_t lane, float* wsc) {
   const uint32_t jn = a.P.J[a.n];
   const uint32_t cnt = a.row_ptr[row + 1] - a.row_ptr[row];
   const float inv = 1.0f / static_cast<float>(cnt);
@@ -167,8 +168,15 @@ __device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const
     float wn = 0.f;
     if (j < jn) {
       float F = 0.f;
+      const float* b = bsn + j * bstride<RP>();
 #pragma unroll
-      for (int r = 0; r < RP; ++r) F = fmaf(bsn[j * bstride<RP>() + r], gg[r], F);
+      for (int r = 0; r < RP; r += 4) {
+        const float4 g4 = get_g(r / 4);
+        F = fmaf(b[r], g4.x, F);
+        F = fmaf(b[r + 1], g4.y, F);
+        F = fmaf(b[r + 2], g4.z, F);
+        F = fmaf(b[r + 3], g4.w, F);
+      }
       const float w = arow[j];
       wn = w - lr * fmaf(F, inv, reg * w);
       bad |= !isfinite(w) || !isfinite(F) || !isfinite(wn);
@@ -206,15 +214,25 @@ __device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
 }
 
-// g held by lane `src` (one-entry-per-lane kernel): broadcast, then the warp
-// row update.
+// g (RP floats) in the warp's shared scratch: broadcast reads.
+template <int RP>
+__device__ __forceinline__ void finalize_row_warp_all(const FactorArgs& a, const float* bsn, uint32_t row,
+                                                      const float* gs, uint32_t lane, float* wsc) {
+  finalize_row_warp_core<RP>(
+      a, bsn, row, [gs](int s) { return reinterpret_cast<const float4*>(gs)[s]; }, lane, wsc);
+}
+
+// g held by lane `src` (one-entry-per-lane kernel, RP <= 12): shuffled into
+// registers, then the warp row update.
 template <int RP>
 __device__ __forceinline__ void finalize_row_warp(const FactorArgs& a, const float* bsn, uint32_t row,
                                                   const float (&g)[RP], int src, uint32_t lane, float* wsc) {
   float gg[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) gg[r] = __shfl_sync(0xffffffffu, g[r], src);
-  finalize_row_warp_all<RP>(a, bsn, row, gg, lane, wsc);
+  finalize_row_warp_core<RP>(
+      a, bsn, row, [&gg](int s) { return make_float4(gg[4 * s], gg[4 * s + 1], gg[4 * s + 2], gg[4 * s + 3]); },
+      lane, wsc);
 }
 
 template <int RP, typename T>
@@ -513,20 +531,10 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
   a.w += b.w;
 }
 
-// All lanes receive the RP components held by group `grp` (4 per lane): one
-// float4 store per group lane into the warp's scratch, then broadcast reads.
-template <int RP>
-__device__ __forceinline__ void group_row(const float4& v, int grp, float (&g)[RP], int gi, int sub, float* gsc) {
-  if (gi == grp) reinterpret_cast<float4*>(gsc)[sub] = v;
+// Group `grp`'s RP components (a float4 per lane) into the warp's scratch.
+__device__ __forceinline__ void group_row(const float4& v, int grp, int gi, int sub, float* gsc) {
   __syncwarp();
-#pragma unroll
-  for (int s = 0; s < RP / 4; ++s) {
-    const float4 o = reinterpret_cast<const float4*>(gsc)[s];
-    g[4 * s] = o.x;
-    g[4 * s + 1] = o.y;
-    g[4 * s + 2] = o.z;
-    g[4 * s + 3] = o.w;
-  }
+  if (gi == grp) reinterpret_cast<float4*>(gsc)[sub] = v;
   __syncwarp();
 }
 
@@ -547,47 +555,48 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
   const bool glane = gi < E;
   const float* Qn = a.P.Q[a.n];
 
-  uint32_t pk = kNone, pi[NO];
-  float px = 0.f;
+  // records of the current step (key, x, ik) and the next one (pk, px, pi);
+  // the current step's Q rows (t, h) were requested one step earlier, so a
+  // step's gathers are in flight while the previous step is reduced
+  uint32_t key = kNone, ik[NO], pk = kNone, pi[NO];
+  float x = 0.f, px = 0.f;
+#pragma unroll
+  for (int j = 0; j < NO; ++j) ik[j] = pi[j] = 0;
   {
     const uint32_t e = ch.begin + gi;
     if (glane && e < ch.end) {
-      pk = ld_stream(a.keys + e);
-      px = ld_stream(a.val + e);
+      key = ld_stream(a.keys + e);
+      x = ld_stream(a.val + e);
 #pragma unroll
-      for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
+      for (int j = 0; j < NO; ++j) ik[j] = ld_stream(a.oidx[j] + e);
+    }
+    const uint32_t e1 = e + E;
+    if (glane && e1 < ch.end) {
+      pk = ld_stream(a.keys + e1);
+      px = ld_stream(a.val + e1);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e1);
     }
   }
-  uint32_t cur = __shfl_sync(kFull, pk, 0);
+  float4 t[NO], h;
+  if (key != kNone) {
+#pragma unroll
+    for (int j = 0; j < NO; ++j)
+      t[j] = __ldg(reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP) + sub);
+    h = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP)[sub];
+  }
+  uint32_t cur = __shfl_sync(kFull, key, 0);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool spread = false;  // acc spread over the groups (else it lives in group carry_g)
   int carry_g = 0;
 
   for (uint32_t base = ch.begin; base < ch.end; base += E) {
-    const uint32_t key = pk;
-    const float x = px;
-    uint32_t ik[NO];
-#pragma unroll
-    for (int j = 0; j < NO; ++j) ik[j] = pi[j];
-    const bool valid = key != kNone;
-    {
-      const uint32_t e = base + E + gi;
-      pk = kNone;
-      if (glane && e < ch.end) {
-        pk = ld_stream(a.keys + e);
-        px = ld_stream(a.val + e);
-#pragma unroll
-        for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
-      }
-    }
+    const uint32_t ckey = key;
+    const float cx = x;
+    const bool valid = ckey != kNone;
     float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
     float p = 0.f;
     if (valid) {
-      float4 t[NO];
-#pragma unroll
-      for (int j = 0; j < NO; ++j)
-        t[j] = __ldg(reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP) + sub);
-      const float4 h = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP)[sub];
       c = t[0];
 #pragma unroll
       for (int j = 1; j < NO; ++j) {
@@ -601,13 +610,34 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
       p = fmaf(h.z, c.z, p);
       p = fmaf(h.w, c.w, p);
     }
+    // advance: request the next step's Q rows, prefetch the records after it
+    key = pk;
+    x = px;
+#pragma unroll
+    for (int j = 0; j < NO; ++j) ik[j] = pi[j];
+    if (key != kNone) {
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+        t[j] = __ldg(reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP) + sub);
+      h = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP)[sub];
+    }
+    {
+      const uint32_t e = base + 2 * E + gi;
+      pk = kNone;
+      if (glane && e < ch.end) {
+        pk = ld_stream(a.keys + e);
+        px = ld_stream(a.val + e);
+#pragma unroll
+        for (int j = 0; j < NO; ++j) pi[j] = ld_stream(a.oidx[j] + e);
+      }
+    }
     p = group_sum<G, Lanes<RP>::kPow2>(p, leader);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (valid) {
-      const float tt = p - x;
+      const float tt = p - cx;
       v = make_float4(tt * c.x, tt * c.y, tt * c.z, tt * c.w);
     }
-    if (__all_sync(kFull, !glane || key == cur)) {
+    if (__all_sync(kFull, !glane || ckey == cur)) {
       add4(acc, v);
       spread = true;
       continue;
@@ -627,31 +657,29 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
     }
 #pragma unroll
     for (int d = 1; d < E; d <<= 1) {  // segmented scan of v over the groups by key
-      const uint32_t okey = __shfl_up_sync(kFull, key, d * G);
+      const uint32_t okey = __shfl_up_sync(kFull, ckey, d * G);
       const float4 o = shfl4_up(v, d * G);
-      if (gi >= d && okey == key) add4(v, o);
+      if (gi >= d && okey == ckey) add4(v, o);
     }
-    const uint32_t nkey = __shfl_down_sync(kFull, key, G);
+    const uint32_t nkey = __shfl_down_sync(kFull, ckey, G);
     const unsigned vmask = __ballot_sync(kFull, valid && sub == 0);
     const int last_g = (31 - __clz(vmask)) / G;
-    const bool seg_end = valid && (gi == E - 1 || nkey != key);
+    const bool seg_end = valid && (gi == E - 1 || nkey != ckey);
     const bool is_last = gi == last_g;
-    if (key == cur) add4(v, tot);
-    const uint32_t key0 = __shfl_sync(kFull, key, 0);
+    if (ckey == cur) add4(v, tot);
+    const uint32_t key0 = __shfl_sync(kFull, ckey, 0);
     if (key0 != cur) {  // the open row ended exactly at the previous step
-      float g[RP];
-      group_row<RP>(tot, 0, g, gi, sub, gsc);
-      finalize_row_warp_all<RP>(a, bsn, cur, g, lane, wsc);
+      group_row(tot, 0, gi, sub, gsc);
+      finalize_row_warp_all<RP>(a, bsn, cur, gsc, lane, wsc);
     }
     unsigned fin = __ballot_sync(kFull, seg_end && !is_last && sub == 0);
     while (fin) {
       const int src = __ffs(fin) - 1;
       fin &= fin - 1;
-      float g[RP];
-      group_row<RP>(v, src / G, g, gi, sub, gsc);
-      finalize_row_warp_all<RP>(a, bsn, __shfl_sync(kFull, key, src), g, lane, wsc);
+      group_row(v, src / G, gi, sub, gsc);
+      finalize_row_warp_all<RP>(a, bsn, __shfl_sync(kFull, ckey, src), gsc, lane, wsc);
     }
-    cur = __shfl_sync(kFull, key, last_g * G);
+    cur = __shfl_sync(kFull, ckey, last_g * G);
     if (is_last) {
       acc = v;
     } else {
@@ -673,14 +701,11 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
   } else {
     tot = shfl4(acc, carry_g * G + sub);
   }
-  float g[RP];
-  group_row<RP>(tot, 0, g, gi, sub, gsc);
+  group_row(tot, 0, gi, sub, gsc);
   if (ch.piece < 0) {
-    finalize_row_warp_all<RP>(a, bsn, cur, g, lane, wsc);
-  } else if (lane == 0) {
-    double* dst = a.piece + static_cast<uint64_t>(ch.piece) * RP;
-#pragma unroll
-    for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(g[r]);
+    finalize_row_warp_all<RP>(a, bsn, cur, gsc, lane, wsc);
+  } else if (lane < RP) {
+    a.piece[static_cast<uint64_t>(ch.piece) * RP + lane] = static_cast<double>(gsc[lane]);
   }
 }
 
