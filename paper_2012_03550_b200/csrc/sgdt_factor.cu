@@ -24,6 +24,8 @@
 // association everywhere -> run-to-run bit identical.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sgdt_internal.cuh"
 
 namespace sgdt {
@@ -758,7 +760,11 @@ int factor_launch(Session& s, FactorArgs& a) {
   const int block = 256, wpb = block / 32;
   if (a.n_chunks) {
     const unsigned grid = (a.n_chunks + wpb - 1) / wpb;
-    if constexpr (RP >= 16)
+    static const bool force_group = [] {
+      const char* e = getenv("SGDT_GROUP_KERNEL");
+      return e && atoi(e) != 0;
+    }();
+    if (RP >= 16 || force_group)
       factor_group_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
     else
       factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);

@@ -12,7 +12,10 @@
 // trainer.cpp:101-103).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -211,6 +214,79 @@ void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, ui
     if (cnt >= kShortRow) cur.pad = 0;  // pad = 1: every row of the chunk is short
   }
   close();
+}
+
+// Intra-row order of the mode-n copy.  The reference visits a row's entries in
+// entry order (CooTensor::mode_perm, sptensor.cpp:102-117); the row's update
+// is a sum over them, so any order is the same row update up to fp32
+// summation order (inside the per-batch tolerance).  Entries of a row are
+// ordered by the coordinate of a secondary mode m: the smallest other mode
+// whose Q table does not fit in L1, so that a warp's gathers of Q^(m) form
+// runs of equal rows (hot Zipf rows coalesce) and sweep the rest in address
+// order.  Ties keep the given order (stable radix sort).  -1: keep the order.
+int secondary_mode(const Session& s, int n) {
+  if (const char* e = std::getenv("SGDT_ROW_ORDER"))
+    if (std::strcmp(e, "entry") == 0) return -1;
+  const uint64_t l1_bytes = 160 * 1024;
+  int best = -1;
+  for (int k = 0; k < s.order; ++k) {
+    if (k == n || static_cast<uint64_t>(s.dims[k]) * s.RP * sizeof(float) <= l1_bytes) continue;
+    if (best < 0 || s.dims[k] < s.dims[best]) best = k;
+  }
+  return best;
+}
+
+__global__ void row_key_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, const uint32_t* __restrict__ perm,
+                               uint64_t len, int n, int m, uint64_t* __restrict__ keys) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < len;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = perm[q];
+    keys[q] = (static_cast<uint64_t>(idx[static_cast<uint64_t>(n) * nnz + e]) << 32) |
+              idx[static_cast<uint64_t>(m) * nnz + e];
+  }
+}
+
+// Re-sorts d_perm[0, len) (a contiguous slice of the mode-n order) by
+// (i_n, i_m); the row grouping and row offsets are unchanged.
+int order_rows_by_secondary(Session& s, int n, uint32_t* d_perm, uint64_t len) {
+  const int m = secondary_mode(s, n);
+  if (m < 0 || len < 2 || len > static_cast<uint64_t>(INT_MAX)) return SGDT_OK;
+  uint64_t *k_in = nullptr, *k_out = nullptr;
+  uint32_t* p_out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int end_bit = 32;
+  while (end_bit < 64 && (1ull << (end_bit - 32)) < s.dims[n]) ++end_bit;
+  int rc = SGDT_OK;
+  auto release = [&] {
+    if (k_in) cudaFree(k_in);
+    if (k_out) cudaFree(k_out);
+    if (p_out) cudaFree(p_out);
+    if (tmp) cudaFree(tmp);
+  };
+  do {
+    if ((rc = dalloc(&k_in, len)) != SGDT_OK) break;
+    if ((rc = dalloc(&k_out, len)) != SGDT_OK) break;
+    if ((rc = dalloc(&p_out, len)) != SGDT_OK) break;
+    row_key_kernel<<<grid_for(len, s.num_sms), 256, 0, s.stream>>>(s.train_rec.idx, s.nnz, d_perm, len, n, m,
+                                                                    k_in);
+    if (cudaGetLastError() != cudaSuccess) {
+      rc = fail(SGDT_ERR_INTERNAL, "row_key_kernel launch failed");
+      break;
+    }
+    if (cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len), 0,
+                                        end_bit, s.stream) != cudaSuccess ||
+        cudaMalloc(&tmp, tmp_bytes) != cudaSuccess ||
+        cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len), 0,
+                                        end_bit, s.stream) != cudaSuccess ||
+        cudaMemcpyAsync(d_perm, p_out, len * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s.stream) != cudaSuccess ||
+        cudaStreamSynchronize(s.stream) != cudaSuccess) {
+      cudaGetLastError();
+      rc = fail(SGDT_ERR_INTERNAL, "intra-row ordering (radix sort) failed");
+    }
+  } while (false);
+  release();
+  return rc;
 }
 
 int upload_record_copy(Session& s, const sgdt_tensor_desc* d, RecordCopy& rc, uint32_t** d_coords_keep,
@@ -594,6 +670,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
       }
       const uint64_t len = qe - qb;
       if (len) SGDT_CUDA(cudaMemcpyAsync(d_perm, hperm + qb, len * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+      TRY(order_rows_by_secondary(*s, n, d_perm, len));
       mp.rec.nnz = len;
       TRY(dalloc(&mp.rec.idx, len * s->order));
       TRY(dalloc(&mp.rec.val, len));
