@@ -394,9 +394,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
-            s.set_model(hA, hB)
-            s.run_epochs(ch, fh, 1)
-            s.get_model((oA, oB))
+            s.run_epochs_host(ch, fh, 1, (hA, hB), (oA, oB))
             hA, oA = oA, hA
             hB, oB = oB, hB
         e1.record(stream)
@@ -404,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
         e_ms = e0.elapsed_time(e1) / args.steps
         e2e = {"value": units * world / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "sgdt_set_model (fp64 pinned host) + sgdt_run_epochs(1) + sgdt_get_model (fp64 pinned host)",
+               "path": "sgdt_run_epochs_host(1): fp64 pinned host model in -> epoch -> fp64 pinned host model out",
                "setup_s": setup_s}
 
     cpu = None

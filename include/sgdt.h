@@ -147,6 +147,18 @@ int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_s
 int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh,
                     uint64_t epochs);
 
+/* The host-model form of sgdt_run_epochs, for callers whose Model lives in
+ * host memory (update_core_epoch / update_factor_epoch take a host Model&,
+ * core_optimizer.cpp:112, factor_optimizer.cpp:101): loads A_in/B_in (fp64,
+ * host), runs `epochs` epochs and writes the final model to A_out/B_out.
+ * Same result as set_model + run_epochs + get_model; the copy-out of B^(k)
+ * overlaps the last factor phase and that of A^(n) overlaps the factor
+ * passes of the modes after n.  A_in/B_in may alias A_out/B_out.  Pinned
+ * host buffers give full PCIe rate. */
+int sgdt_run_epochs_host(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh,
+                         uint64_t epochs, const double* const* A_in, const double* const* B_in,
+                         double* const* A_out, double* const* B_out);
+
 /* rmse_mae (eval.cpp:15-33) over the training (which=0) or test (which=1)
  * entries of the session, fp64 accumulation, fixed summation order. */
 int sgdt_eval(sgdt_session* s, int which, double* rmse, double* mae);

@@ -158,6 +158,8 @@ struct Session {
 
   double* stage = nullptr;  // fp64 staging for model transfer
   uint64_t stage_cap = 0;
+  double* xfer = nullptr;  // fp64 staging of the whole model (sgdt_run_epochs_host)
+  uint64_t xfer_cap = 0;
 
   cudaEvent_t ev[4 + kMaxOrder] = {};
   sgdt_timing timing{};

@@ -225,13 +225,16 @@ void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, ui
 // runs of equal rows (hot Zipf rows coalesce) and sweep the rest in address
 // order.  Ties keep the given order (stable radix sort).  -1: keep the order.
 int secondary_mode(const Session& s, int n) {
-  if (const char* e = std::getenv("SGDT_ROW_ORDER"))
+  bool largest = false;
+  if (const char* e = std::getenv("SGDT_ROW_ORDER")) {  // diagnostics: entry | largest
     if (std::strcmp(e, "entry") == 0) return -1;
+    largest = std::strcmp(e, "largest") == 0;
+  }
   const uint64_t l1_bytes = 160 * 1024;
   int best = -1;
   for (int k = 0; k < s.order; ++k) {
     if (k == n || static_cast<uint64_t>(s.dims[k]) * s.RP * sizeof(float) <= l1_bytes) continue;
-    if (best < 0 || s.dims[k] < s.dims[best]) best = k;
+    if (best < 0 || (largest ? s.dims[k] > s.dims[best] : s.dims[k] < s.dims[best])) best = k;
   }
   return best;
 }
@@ -366,6 +369,7 @@ void free_session(sgdt_session* s) {
   F(s->ev_out);
   F(s->flag);
   F(s->stage);
+  F(s->xfer);
   if (s->h_ev_out) cudaFreeHost(s->h_ev_out);
   if (s->h_flag) cudaFreeHost(s->h_flag);
   for (auto& e : s->ev)
@@ -628,7 +632,12 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
   s->num_sms = prop.multiProcessorCount;
   int rc = [&]() -> int {
     SGDT_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    SGDT_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    // the side stream (run-ahead sampler, model copy-out) has the highest
+    // priority so its short kernels are dispatched between the blocks of the
+    // factor kernels instead of after them
+    int prio_lo = 0, prio_hi = 0;
+    SGDT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SGDT_CUDA(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
     for (auto& e : s->ev) SGDT_CUDA(cudaEventCreate(&e));
     for (cudaEvent_t* e : {&s->ev_start, &s->ev_core, &s->ev_samp})
       SGDT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -897,7 +906,81 @@ int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_s
   return sync_and_flag(*s);
 }
 
+}  // extern "C"
+
+namespace sgdt {
+namespace {
+// Host destinations of the final model (sgdt_run_epochs_host); offsets into
+// Session::xfer per matrix.
+struct CopyOut {
+  double* const* A;
+  double* const* B;
+  uint64_t offA[kMaxOrder], offB[kMaxOrder];
+};
+
+int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
+                    const CopyOut* out);
+}  // namespace
+}  // namespace sgdt
+
+extern "C" {
+
 int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs) {
+  return run_epochs_impl(s, ch, fh, epochs, nullptr);
+}
+
+int sgdt_run_epochs_host(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
+                         const double* const* A_in, const double* const* B_in, double* const* A_out,
+                         double* const* B_out) {
+  if (!s || !A_in || !B_in || !A_out || !B_out) return fail(SGDT_ERR_DOMAIN, "run_epochs_host: null argument");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, ch, &m));
+  TRY(check_factor_hyper(fh));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  CopyOut co{A_out, B_out, {}, {}};
+  uint64_t total = 0;
+  for (int k = 0; k < s->order; ++k) {
+    co.offA[k] = total;
+    total += static_cast<uint64_t>(s->dims[k]) * s->J[k];
+    co.offB[k] = total;
+    total += static_cast<uint64_t>(s->J[k]) * s->R;
+  }
+  if (total > s->xfer_cap) {
+    if (s->xfer) cudaFree(s->xfer);
+    s->xfer = nullptr;
+    s->xfer_cap = 0;
+    TRY(dalloc(&s->xfer, total));
+    s->xfer_cap = total;
+  }
+  // load: the copies back to back, then the casts
+  for (int k = 0; k < s->order; ++k) {
+    const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k], nb = static_cast<uint64_t>(s->J[k]) * s->R;
+    SGDT_CUDA(cudaMemcpyAsync(s->xfer + co.offA[k], A_in[k], na * sizeof(double), cudaMemcpyHostToDevice,
+                              s->stream));
+    SGDT_CUDA(cudaMemcpyAsync(s->xfer + co.offB[k], B_in[k], nb * sizeof(double), cudaMemcpyHostToDevice,
+                              s->stream));
+  }
+  for (int k = 0; k < s->order; ++k) {
+    const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k], nb = static_cast<uint64_t>(s->J[k]) * s->R;
+    cast_d2f_kernel<<<grid_for(na, s->num_sms), 256, 0, s->stream>>>(s->xfer + co.offA[k], s->P.A[k], na);
+    cast_d2f_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->xfer + co.offB[k], s->P.B[k], nb);
+    SGDT_CUDA(cudaGetLastError());
+    s->launches += 2;
+  }
+  for (int k = 0; k < s->order; ++k) TRY(launch_q_refresh(*s, k));
+  if (epochs == 0) {
+    SGDT_CUDA(cudaStreamSynchronize(s->stream));
+    return sgdt_get_model(s, A_out, B_out);
+  }
+  return run_epochs_impl(s, ch, fh, epochs, &co);
+}
+
+}  // extern "C"
+
+namespace sgdt {
+namespace {
+int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
+                    const CopyOut* out) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   uint64_t m = 0;
   TRY(check_core_hyper(*s, ch, &m));
@@ -936,7 +1019,32 @@ int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
     TRY(enqueue_factor(*s, *fh, last));
     if (last) SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
   }
-  TRY(sync_and_flag(*s));
+  if (out) {
+    // copy-out on the side stream: B^(k) is final after the last core phase,
+    // A^(n) after the last factor pass of mode n
+    const bool modes = fh->lr > 0.0;
+    SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev[1], 0));
+    for (int k = 0; k < s->order; ++k) {
+      const uint64_t nb = static_cast<uint64_t>(s->J[k]) * s->R;
+      cast_f2d_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->side>>>(s->P.B[k], s->xfer + out->offB[k], nb);
+      SGDT_CUDA(cudaMemcpyAsync(out->B[k], s->xfer + out->offB[k], nb * sizeof(double), cudaMemcpyDeviceToHost,
+                                s->side));
+    }
+    for (int n = 0; n < s->order; ++n) {
+      const uint64_t na = static_cast<uint64_t>(s->dims[n]) * s->J[n];
+      SGDT_CUDA(cudaStreamWaitEvent(s->side, modes && n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2], 0));
+      cast_f2d_kernel<<<grid_for(na, s->num_sms), 256, 0, s->side>>>(s->P.A[n], s->xfer + out->offA[n], na);
+      SGDT_CUDA(cudaMemcpyAsync(out->A[n], s->xfer + out->offA[n], na * sizeof(double), cudaMemcpyDeviceToHost,
+                                s->side));
+    }
+    SGDT_CUDA(cudaGetLastError());
+    s->launches += 2 * s->order;
+  }
+  {
+    const int rc = sync_and_flag(*s);
+    if (out) SGDT_CUDA(cudaStreamSynchronize(s->side));
+    if (rc != SGDT_OK) return rc;
+  }
   sgdt_timing t{};
   SGDT_CUDA(cudaEventElapsedTime(&t.core_ms, s->ev[0], s->ev[1]));
   SGDT_CUDA(cudaEventElapsedTime(&t.factor_ms, s->ev[1], s->ev[2]));
@@ -948,6 +1056,11 @@ int sgdt_run_epochs(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
   s->timing_valid = true;
   return SGDT_OK;
 }
+
+}  // namespace
+}  // namespace sgdt
+
+extern "C" {
 
 int sgdt_eval(sgdt_session* s, int which, double* rmse, double* mae) {
   if (!s || !rmse || !mae) return fail(SGDT_ERR_DOMAIN, "null argument");

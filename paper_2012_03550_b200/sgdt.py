@@ -118,6 +118,7 @@ def load(build_if_missing: bool = True):
     L.sgdt_core_epoch.argtypes = [vp, C.POINTER(CoreHyper), C.POINTER(_CoreStats)]
     L.sgdt_factor_epoch.argtypes = [vp, C.POINTER(FactorHyper), C.POINTER(_FactorStats)]
     L.sgdt_run_epochs.argtypes = [vp, C.POINTER(CoreHyper), C.POINTER(FactorHyper), C.c_uint64]
+    L.sgdt_run_epochs_host.argtypes = [vp, C.POINTER(CoreHyper), C.POINTER(FactorHyper), C.c_uint64, dpp, dpp, dpp, dpp]
     L.sgdt_eval.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.sgdt_train.argtypes = [vp, C.POINTER(CoreHyper), C.POINTER(FactorHyper), C.c_uint64,
                              C.POINTER(C.c_double)]
@@ -288,6 +289,21 @@ class Session:
 
     def run_epochs(self, core: CoreHyper, factor: FactorHyper, epochs: int = 1) -> None:
         _ck(_lib.sgdt_run_epochs(self.h, C.byref(core), C.byref(factor), epochs))
+
+    def run_epochs_host(self, core: CoreHyper, factor: FactorHyper, epochs: int, model_in, model_out=None):
+        """sgdt_run_epochs_host: host fp64 model in, `epochs` epochs, host fp64
+        model out (model_out may be model_in; pinned buffers copy fastest)."""
+        A, B = model_in
+        for x in list(A) + list(B):
+            if x.dtype != np.float64 or not x.flags.c_contiguous:
+                raise DataError("run_epochs_host: model arrays must be C-contiguous float64")
+        if model_out is None:
+            model_out = ([np.empty_like(a) for a in A], [np.empty_like(b) for b in B])
+        oA, oB = model_out
+        ptrs = lambda xs: (C.c_void_p * MAX_ORDER)(*[x.ctypes.data for x in xs])
+        _ck(_lib.sgdt_run_epochs_host(self.h, C.byref(core), C.byref(factor), epochs, ptrs(A), ptrs(B), ptrs(oA),
+                                      ptrs(oB)))
+        return oA, oB
 
     def eval(self, which: int = 0):
         a, b = C.c_double(), C.c_double()

@@ -305,6 +305,34 @@ def test_run_to_run_bit_identical():
         assert np.array_equal(outs[0][1][n], outs[1][1][n])
 
 
+@pytest.mark.parametrize("factor_lr", [0.01, 0.0])
+def test_run_epochs_host_matches_set_run_get(factor_lr):
+    """sgdt_run_epochs_host (host model in, overlapped copy-out) is exactly
+    set_model + run_epochs + get_model, including with the outputs aliasing
+    the inputs and with the factor phase frozen."""
+    dims, J, R = (60, 300, 40), (8, 8, 8), 8
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, R, 20000, 5, tm=0.0, ts=sig)
+    ch, fh = sg().CoreHyper(0.01, 0.01, 1024, 0, 0), sg().FactorHyper(factor_lr, 0.01, 1.0)
+    m = oracle_model(dims, J, R, 3, sd=sig, mean=0.0)
+    A0, B0 = m.params()
+    a = session_for(dims, tr, J, R)
+    a.set_model(A0, B0)
+    a.seed(5)
+    a.run_epochs(ch, fh, 2)
+    want = a.get_model()
+    b = session_for(dims, tr, J, R)
+    b.seed(5)
+    got = b.run_epochs_host(ch, fh, 2, ([x.copy() for x in A0], [x.copy() for x in B0]))
+    c = session_for(dims, tr, J, R)
+    c.seed(5)
+    io = ([x.copy() for x in A0], [x.copy() for x in B0])
+    c.run_epochs_host(ch, fh, 2, io, io)
+    for n in range(3):
+        for res in (got, io):
+            assert np.array_equal(res[0][n], want[0][n]) and np.array_equal(res[1][n], want[1][n])
+
+
 def test_run_epochs_pipelined_sampler_matches_oracle():
     """sgdt_run_epochs draws epoch e+1's Psi on a side stream during epoch e's
     factor phase; the RNG stream, the pool and every Psi must still be exactly
