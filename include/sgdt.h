@@ -222,6 +222,46 @@ int sgdt_refresh_q(sgdt_session* s, int mode);
 /* Wait for all work of the session (both of its streams). */
 int sgdt_synchronize(sgdt_session* s);
 
+/* ---- peer-memory publication of the sharded factor phase ----------------
+ * Replaces the host round trip of the boundary merge and the row-block
+ * broadcast (factor_optimizer.cpp:247-270 plus the all-gather of A^(n)):
+ * after sgdt_set_peers, every row the factor kernels finalise is stored into
+ * the local A^(n)/Q^(n) and into every peer's copy (NVLink P2P stores from
+ * the finaliser), and the export record of the cut rows is stored into every
+ * peer's record slot.  The caller orders the ranks with a barrier after
+ * sgdt_factor_mode_p2p and after sgdt_factor_merge_p2p (a stream-ordered
+ * collective or a host barrier after sgdt_synchronize). */
+
+/* This session's peer-visible buffers, 2N+1 device pointers: A^(0..N-1),
+ * Q^(0..N-1), the export-record slots. */
+int sgdt_peer_buffers(sgdt_session* s, void** ptrs);
+/* The same buffers as CUDA IPC handles (2N+1 x 64 bytes), for peers in other
+ * processes; sgdt_ipc_open maps one into the calling process. */
+int sgdt_peer_ipc_handles(sgdt_session* s, void* handles);
+int sgdt_ipc_open(const void* handle, int device, void** ptr);
+/* Install every rank's buffers: ptrs is world x (2N+1) pointers valid in this
+ * process, rank-major (this rank's own row is ignored). */
+int sgdt_set_peers(sgdt_session* s, const void* const* ptrs);
+/* Replicated core phase without a host synchronisation (the numeric flag is
+ * checked by sgdt_check). */
+int sgdt_core_epoch_async(sgdt_session* s, const sgdt_core_hyper* h);
+/* Draw the NEXT core phase's Psi now, on the side stream, overlapped with the
+ * rest of this epoch (Psi does not depend on the model).  The RNG and pool
+ * advance immediately, exactly as the next core phase would advance them;
+ * the next sgdt_core_epoch_async (same hyper-parameters) consumes the draw.
+ * Until then other RNG consumers are refused and RNG/pool setters discard it. */
+int sgdt_sample_ahead(sgdt_session* s, const sgdt_core_hyper* h);
+/* Factor pass of `mode` over this rank's slice with peer stores, then this
+ * rank's export record {n_export, row0, row1, g0[RP], g1[RP]} into slot
+ * `rank` of every rank's record buffer.  Asynchronous. */
+int sgdt_factor_mode_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h);
+/* After every rank's sgdt_factor_mode_p2p: rank-ordered fp64 merge of the
+ * records and the owner's finalisation of the cut row it publishes (peer
+ * stores included).  Asynchronous. */
+int sgdt_factor_merge_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h);
+/* Synchronise and check the numeric flag (SGDT_ERR_NUMERIC on divergence). */
+int sgdt_check(sgdt_session* s);
+
 /* Device next_below over an explicit MT state (test hook for the rejection
  * path, rng.hpp:20-25): draws n values with bounds[i] sequentially. */
 int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,

@@ -52,6 +52,7 @@ struct FactorArgs {
   uint64_t qbase;  // row_ptr value of the copy's first record (shard slice start)
   double lr, reg;
   int* flag;
+  const PeerTable* peers;  // null: single device; else the peers' A^(n)/Q^(n) (stores ride along)
 };
 
 // Streamed record loads: read once, never reused -> keep them out of L1,
@@ -96,6 +97,7 @@ struct RowUpdate {
   uint32_t jn;
   float lr, reg;
   int* flag;
+  const PeerTable* peers;
 };
 
 // F = B^(n) g; a -= lr (F/cnt + reg a); Q^(n)[row] = a B^(n).  One lane, fp32
@@ -119,6 +121,8 @@ __device__ __noinline__ void finalize_row_impl(RowUpdate u, uint32_t row, const 
     const float wn = w - u.lr * fmaf(F, inv, u.reg * w);
     bad |= !isfinite(wn);
     arow[j] = wn;
+    if (u.peers)
+      for (int p = 0; p < u.peers->n; ++p) u.peers->A[p][static_cast<uint64_t>(row) * u.jn + j] = wn;
   }
   float4* dst = reinterpret_cast<float4*>(u.Q + static_cast<uint64_t>(row) * RP);
 #pragma unroll 1
@@ -133,13 +137,16 @@ __device__ __noinline__ void finalize_row_impl(RowUpdate u, uint32_t row, const 
       q.w = fmaf(wf, b[3], q.w);
     }
     dst[s] = q;
+    if (u.peers)
+      for (int p = 0; p < u.peers->n; ++p)
+        reinterpret_cast<float4*>(u.peers->Q[p] + static_cast<uint64_t>(row) * RP)[s] = q;
   }
   if (bad) atomicOr(u.flag, 8);
 }
 
 __device__ __forceinline__ RowUpdate row_update(const FactorArgs& a, const float* bsn) {
   return RowUpdate{a.P.A[a.n], a.P.Q[a.n], a.row_ptr, bsn, a.P.J[a.n], static_cast<float>(a.lr),
-                   static_cast<float>(a.reg), a.flag};
+                   static_cast<float>(a.reg), a.flag, a.peers};
 }
 
 template <int RP, typename T>
@@ -183,6 +190,8 @@ __device__ __forceinline__ void finalize_row_warp_core(const FactorArgs& a, cons
       wn = w - lr * fmaf(F, inv, reg * w);
       bad |= !isfinite(w) || !isfinite(F) || !isfinite(wn);
       arow[j] = wn;
+      if (a.peers)
+        for (int p = 0; p < a.peers->n; ++p) a.peers->A[p][static_cast<uint64_t>(row) * jn + j] = wn;
     }
     if constexpr (RP <= 12) {  // narrow rows: J shuffles are cheaper than the scratch round trip
       const uint32_t jend = jn - j0 < 32 ? jn - j0 : 32;
@@ -195,7 +204,11 @@ __device__ __forceinline__ void finalize_row_warp_core(const FactorArgs& a, cons
     }
   }
   if constexpr (RP <= 12) {
-    if (lane < RP) a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+    if (lane < RP) {
+      a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+      if (a.peers)
+        for (int p = 0; p < a.peers->n; ++p) a.peers->Q[p][static_cast<uint64_t>(row) * RP + lane] = q;
+    }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
     return;
   }
@@ -211,6 +224,8 @@ __device__ __forceinline__ void finalize_row_warp_core(const FactorArgs& a, cons
       q = fmaf(w4.w, b[3 * bstride<RP>()], q);
     }
     a.P.Q[a.n][static_cast<uint64_t>(row) * RP + lane] = q;
+    if (a.peers)
+      for (int p = 0; p < a.peers->n; ++p) a.peers->Q[p][static_cast<uint64_t>(row) * RP + lane] = q;
   }
   __syncwarp();
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 8);
@@ -832,6 +847,7 @@ FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h, bool subse
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;
+  a.peers = s.npeers > 0 ? s.d_peers + n : nullptr;
   return a;
 }
 

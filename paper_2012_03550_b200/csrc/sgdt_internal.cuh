@@ -53,6 +53,17 @@ struct ShardPlan {
   uint32_t export_rows[2] = {0, 0};
 };
 
+// Peer-memory publication (sharded factor phase): the other ranks' copies of
+// A^(n) and Q^(n), into which every finalised row is also stored, so the
+// row all-gather rides on the finaliser's own stores (NVLink P2P).
+constexpr int kMaxPeers = 7;
+struct PeerTable {
+  int n;
+  int pad;
+  float* A[kMaxPeers];
+  float* Q[kMaxPeers];
+};
+
 struct RecordCopy {
   uint32_t* idx = nullptr;  // order x nnz
   float* val = nullptr;     // nnz
@@ -123,6 +134,17 @@ struct Session {
   double* piece_partials = nullptr;  // max pieces x RP
   double* export_buf = nullptr;      // 2 x RP, boundary-row partials of the last mode run
 
+  // peer publication (sgdt_set_peers): per-mode peer tables on the device,
+  // the export-record slots (world x rec_stride fp64, slot = rank) and the
+  // peers' record buffers
+  PeerTable* d_peers = nullptr;  // kMaxOrder tables
+  int npeers = 0;
+  uint32_t rec_stride = 0;       // 3 + 2 RP: {n_export, row0, row1, g0[RP], g1[RP]}
+  double* xrec = nullptr;
+  double* peer_rec[kMaxPeers] = {};
+  uint32_t* merge_rows = nullptr;  // 2
+  double* merge_g = nullptr;       // 2 x RP
+
   // sampler state
   uint64_t* mt = nullptr;       // 312 words + position word
   uint32_t* pool = nullptr;     // nnz, persistent
@@ -138,6 +160,12 @@ struct Session {
   uint64_t batch_cap = 0;
   uint64_t last_batch_len = 0;
   uint32_t* last_batch = nullptr;  // points into batch
+  // sgdt_sample_ahead: the next core phase's Psi, drawn on the side stream
+  bool ahead_valid = false;
+  uint64_t ahead_m = 0;
+  int ahead_per_mode = 0;
+  int ahead_slot = 0;      // batch slot holding it
+  int core_slot = 0;       // batch slot read by the last enqueued core phase
 
   // core scratch (M samples)
   float* cs_a = nullptr;      // M x Jmax

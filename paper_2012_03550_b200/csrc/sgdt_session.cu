@@ -292,6 +292,43 @@ int order_rows_by_secondary(Session& s, int n, uint32_t* d_perm, uint64_t len) {
   return rc;
 }
 
+// This rank's export record {n_export, row0, row1, g0[RP], g1[RP]} into slot
+// `rank` of every rank's record buffer (local and peers, P2P stores).
+struct RecordDst {
+  double* p[kMaxPeers + 1];
+  int n;
+};
+__global__ void publish_record_kernel(const double* __restrict__ xport, uint32_t n_export, uint32_t row0,
+                                      uint32_t row1, uint32_t stride, int rank, RecordDst dst) {
+  for (uint32_t i = threadIdx.x; i < stride; i += blockDim.x) {
+    const double v = i == 0 ? static_cast<double>(n_export)
+                            : (i == 1 ? static_cast<double>(row0) : (i == 2 ? static_cast<double>(row1) : xport[i - 3]));
+    for (int d = 0; d < dst.n; ++d) dst.p[d][static_cast<uint64_t>(rank) * stride + i] = v;
+  }
+}
+
+// Rank-ordered merge of the records for up to 2 rows this rank finalises
+// (merge_boundary of the host driver, on the device): g[i] = sum over ranks
+// ascending, over their slots in order, of the partials of rows[i].
+__global__ void merge_records_kernel(const double* __restrict__ rec, int world, uint32_t stride, uint32_t RP,
+                                     uint32_t k, uint32_t row0, uint32_t row1, uint32_t* rows_out,
+                                     double* g_out) {
+  const uint32_t t = threadIdx.x;
+  if (t < k) rows_out[t] = t == 0 ? row0 : row1;
+  for (uint32_t x = t; x < k * RP; x += blockDim.x) {
+    const uint32_t i = x / RP, r = x % RP;
+    const double row = static_cast<double>(i == 0 ? row0 : row1);
+    double g = 0.0;
+    for (int w = 0; w < world; ++w) {
+      const double* R0 = rec + static_cast<uint64_t>(w) * stride;
+      const uint32_t ne = static_cast<uint32_t>(R0[0]);
+      for (uint32_t q = 0; q < ne && q < 2; ++q)
+        if (R0[1 + q] == row) g += R0[3 + q * RP + r];
+    }
+    g_out[x] = g;
+  }
+}
+
 int upload_record_copy(Session& s, const sgdt_tensor_desc* d, RecordCopy& rc, uint32_t** d_coords_keep,
                        double** d_values_keep) {
   const uint64_t nnz = d->nnz;
@@ -351,6 +388,10 @@ void free_session(sgdt_session* s) {
   }
   F(s->piece_partials);
   F(s->export_buf);
+  F(s->xrec);
+  F(s->merge_rows);
+  F(s->merge_g);
+  F(s->d_peers);
   F(s->mt);
   F(s->pool);
   F(s->head);
@@ -465,6 +506,7 @@ int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_
   TRY(ensure_core_capacity(s, m));
   const bool per_mode = h.resample_per_mode && h.batch_m != 0;
   const uint32_t* batch = presampled;
+  s.core_slot = presampled && presampled != s.batch ? 1 : 0;
   if (!batch) {
     if (h.batch_m == 0) {
       iota32_kernel<<<grid_for(m, s.num_sms), 256, 0, s.stream>>>(s.batch, m);
@@ -557,6 +599,19 @@ int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
     TRY(launch_factor_mode(s, n, h, subset));
   }
   return SGDT_OK;
+}
+
+// A pending sgdt_sample_ahead draw: setters discard it (the state they
+// install replaces the RNG/pool it advanced); other RNG consumers would draw
+// out of the reference order, so they are refused until a core phase takes it.
+int settle_ahead(Session& s, bool discard, const char* who) {
+  if (!s.ahead_valid) return SGDT_OK;
+  SGDT_CUDA(cudaStreamSynchronize(s.side));
+  if (discard) {
+    s.ahead_valid = false;
+    return SGDT_OK;
+  }
+  return fail(SGDT_ERR_CONFIG, std::string(who) + ": a sgdt_sample_ahead draw is pending; run sgdt_core_epoch_async first");
 }
 
 int sync_and_flag(Session& s) {
@@ -735,6 +790,11 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     s->piece_cap = std::max<uint32_t>(max_pieces, 1);
     TRY(dalloc(&s->piece_partials, static_cast<uint64_t>(s->piece_cap) * s->RP));
     TRY(dalloc(&s->export_buf, 2ull * s->RP));
+    s->rec_stride = 3 + 2 * s->RP;
+    TRY(dalloc(&s->xrec, static_cast<uint64_t>(world) * s->rec_stride));
+    TRY(dalloc(&s->merge_rows, 2));
+    TRY(dalloc(&s->merge_g, 2ull * s->RP));
+    TRY(dalloc(&s->d_peers, kMaxOrder));
     // sampler
     TRY(dalloc(&s->mt, 313));
     uint64_t mt[313];
@@ -807,6 +867,7 @@ int sgdt_set_rng(sgdt_session* s, const uint64_t* mt312, uint32_t pos) {
   if (!s || !mt312) return fail(SGDT_ERR_DOMAIN, "set_rng: null argument");
   if (pos > 312) return fail(SGDT_ERR_DOMAIN, "set_rng: position out of range");
   SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(settle_ahead(*s, true, "set_rng"));
   uint64_t st[313];
   std::memcpy(st, mt312, 312 * sizeof(uint64_t));
   st[312] = pos;
@@ -818,6 +879,7 @@ int sgdt_set_rng(sgdt_session* s, const uint64_t* mt312, uint32_t pos) {
 int sgdt_get_rng(sgdt_session* s, uint64_t* mt312, uint32_t* pos) {
   if (!s || !mt312 || !pos) return fail(SGDT_ERR_DOMAIN, "get_rng: null argument");
   SGDT_CUDA(cudaSetDevice(s->device));
+  SGDT_CUDA(cudaStreamSynchronize(s->side));
   uint64_t st[313];
   SGDT_CUDA(cudaMemcpyAsync(st, s->mt, sizeof st, cudaMemcpyDeviceToHost, s->stream));
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
@@ -828,6 +890,7 @@ int sgdt_get_rng(sgdt_session* s, uint64_t* mt312, uint32_t* pos) {
 
 int sgdt_reset_pool(sgdt_session* s) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  TRY(settle_ahead(*s, true, "reset_pool"));
   s->pool_valid = false;
   return SGDT_OK;
 }
@@ -835,6 +898,7 @@ int sgdt_reset_pool(sgdt_session* s) {
 int sgdt_set_pool(sgdt_session* s, const uint32_t* pool) {
   if (!s || !pool) return fail(SGDT_ERR_DOMAIN, "set_pool: null argument");
   SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(settle_ahead(*s, true, "set_pool"));
   SGDT_CUDA(cudaMemcpyAsync(s->pool, pool, s->nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
   s->pool_valid = true;
@@ -844,6 +908,7 @@ int sgdt_set_pool(sgdt_session* s, const uint32_t* pool) {
 int sgdt_get_pool(sgdt_session* s, uint32_t* pool) {
   if (!s || !pool) return fail(SGDT_ERR_DOMAIN, "get_pool: null argument");
   SGDT_CUDA(cudaSetDevice(s->device));
+  SGDT_CUDA(cudaStreamSynchronize(s->side));
   if (!s->pool_valid) {
     for (uint64_t e = 0; e < s->nnz; ++e) pool[e] = static_cast<uint32_t>(e);
     return SGDT_OK;
@@ -857,6 +922,7 @@ int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   if (m < 1 || m > s->nnz) return fail(SGDT_ERR_DOMAIN, "sample_batch: batch size out of range");
   SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(settle_ahead(*s, false, "sample_batch"));
   TRY(ensure_batch_capacity(*s, m));
   TRY(launch_sampler(*s, m, s->batch, s->stream));
   if (out) SGDT_CUDA(cudaMemcpyAsync(out, s->batch, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
@@ -866,6 +932,7 @@ int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
 
 int sgdt_last_batch(sgdt_session* s, uint32_t* out, uint64_t* len) {
   if (!s || !len) return fail(SGDT_ERR_DOMAIN, "null argument");
+  SGDT_CUDA(cudaStreamSynchronize(s->side));
   *len = s->last_batch_len;
   if (out && s->last_batch_len) {
     SGDT_CUDA(cudaMemcpyAsync(out, s->last_batch, s->last_batch_len * sizeof(uint32_t), cudaMemcpyDeviceToHost,
@@ -885,6 +952,7 @@ int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* 
     st->effective_workers = h->lr == 0.0 ? 0 : 1;
   }
   if (h->lr == 0.0) return SGDT_OK;
+  TRY(settle_ahead(*s, false, "core_epoch"));
   TRY(enqueue_core(*s, *h, m));
   return sync_and_flag(*s);
 }
@@ -902,6 +970,7 @@ int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_s
       }
   }
   if (h->lr == 0.0) return SGDT_OK;
+  if (h->row_fraction < 1.0) TRY(settle_ahead(*s, false, "factor_epoch (row_fraction < 1)"));
   TRY(enqueue_factor(*s, *h, false));
   return sync_and_flag(*s);
 }
@@ -986,6 +1055,7 @@ int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
   TRY(check_core_hyper(*s, ch, &m));
   TRY(check_factor_hyper(fh));
   SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(settle_ahead(*s, false, "run_epochs"));
   if (epochs == 0) return SGDT_OK;
   // Psi does not depend on the model, so epoch e+1's sampler runs on the side
   // stream during epoch e's factor phase (double-buffered Psi).  The RNG
@@ -1186,6 +1256,146 @@ int sgdt_refresh_q(sgdt_session* s, int mode) {
   TRY(launch_q_refresh(*s, mode));
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
   return SGDT_OK;
+}
+
+int sgdt_peer_buffers(sgdt_session* s, void** ptrs) {
+  if (!s || !ptrs) return fail(SGDT_ERR_DOMAIN, "null argument");
+  for (int k = 0; k < s->order; ++k) {
+    ptrs[k] = s->P.A[k];
+    ptrs[s->order + k] = s->P.Q[k];
+  }
+  ptrs[2 * s->order] = s->xrec;
+  return SGDT_OK;
+}
+
+int sgdt_peer_ipc_handles(sgdt_session* s, void* handles) {
+  if (!s || !handles) return fail(SGDT_ERR_DOMAIN, "null argument");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  void* ptrs[2 * kMaxOrder + 1];
+  TRY(sgdt_peer_buffers(s, ptrs));
+  auto* out = static_cast<cudaIpcMemHandle_t*>(handles);
+  for (int i = 0; i < 2 * s->order + 1; ++i) SGDT_CUDA(cudaIpcGetMemHandle(&out[i], ptrs[i]));
+  return SGDT_OK;
+}
+
+int sgdt_ipc_open(const void* handle, int device, void** ptr) {
+  if (!handle || !ptr) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (device >= 0) SGDT_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  SGDT_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SGDT_OK;
+}
+
+int sgdt_set_peers(sgdt_session* s, const void* const* ptrs) {
+  if (!s || !ptrs) return fail(SGDT_ERR_DOMAIN, "null argument");
+  if (s->world - 1 > kMaxPeers) return fail(SGDT_ERR_CONFIG, "set_peers: at most 8 ranks");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  const int per = 2 * s->order + 1;
+  PeerTable tab[kMaxOrder] = {};
+  int np = 0;
+  for (int r = 0; r < s->world; ++r) {
+    if (r == s->rank) continue;
+    const void* const* row = ptrs + static_cast<size_t>(r) * per;
+    for (int k = 0; k < s->order; ++k) {
+      tab[k].A[np] = static_cast<float*>(const_cast<void*>(row[k]));
+      tab[k].Q[np] = static_cast<float*>(const_cast<void*>(row[s->order + k]));
+    }
+    s->peer_rec[np] = static_cast<double*>(const_cast<void*>(row[2 * s->order]));
+    ++np;
+  }
+  for (int k = 0; k < s->order; ++k) tab[k].n = np;
+  SGDT_CUDA(cudaMemcpyAsync(s->d_peers, tab, sizeof tab, cudaMemcpyHostToDevice, s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  s->npeers = np;
+  return SGDT_OK;
+}
+
+int sgdt_core_epoch_async(sgdt_session* s, const sgdt_core_hyper* h) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, h, &m));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  const int per_mode = h->resample_per_mode && h->batch_m != 0 ? 1 : 0;
+  if (s->ahead_valid) {
+    if (h->lr == 0.0 || s->ahead_m != m || s->ahead_per_mode != per_mode)
+      return fail(SGDT_ERR_CONFIG, "core_epoch_async: hyper-parameters differ from the pending sgdt_sample_ahead");
+    s->ahead_valid = false;
+    SGDT_CUDA(cudaStreamWaitEvent(s->stream, s->ev_samp, 0));
+    return enqueue_core(*s, *h, m, s->batch + static_cast<uint64_t>(s->ahead_slot) * s->order * m);
+  }
+  if (h->lr == 0.0) return SGDT_OK;
+  return enqueue_core(*s, *h, m);
+}
+
+int sgdt_sample_ahead(sgdt_session* s, const sgdt_core_hyper* h) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, h, &m));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (s->ahead_valid) return fail(SGDT_ERR_CONFIG, "sample_ahead: a draw is already pending");
+  if (h->lr == 0.0 || h->batch_m == 0) return SGDT_OK;  // that core phase draws nothing
+  TRY(ensure_batch_capacity(*s, m));
+  TRY(ensure_core_capacity(*s, m));
+  s->ahead_slot = 1 - s->core_slot;  // the slot the enqueued core phase is not reading
+  SGDT_CUDA(cudaEventRecord(s->ev_core, s->stream));
+  SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_core, 0));
+  TRY(enqueue_sample(*s, *h, m, s->batch + static_cast<uint64_t>(s->ahead_slot) * s->order * m, s->side));
+  SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+  s->ahead_valid = true;
+  s->ahead_m = m;
+  s->ahead_per_mode = h->resample_per_mode ? 1 : 0;
+  return SGDT_OK;
+}
+
+int sgdt_factor_mode_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_mode_p2p: mode out of range");
+  TRY(check_factor_hyper(h));
+  if (h->lr > 0.0 && h->row_fraction < 1.0)
+    return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not supported by the sharded (multi-GPU) factor phase");
+  if (s->world > 1 && s->npeers != s->world - 1) return fail(SGDT_ERR_CONFIG, "factor_mode_p2p: peers not set");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (h->lr == 0.0) return SGDT_OK;
+  TRY(launch_factor_mode(*s, mode, *h));
+  const ShardPlan& sp = s->mode[mode].shard;
+  RecordDst dst{};
+  dst.p[0] = s->xrec;
+  for (int p = 0; p < s->npeers; ++p) dst.p[1 + p] = s->peer_rec[p];
+  dst.n = 1 + s->npeers;
+  publish_record_kernel<<<1, 128, 0, s->stream>>>(s->export_buf, sp.n_export, sp.export_rows[0],
+                                                  sp.export_rows[1], s->rec_stride, s->rank, dst);
+  SGDT_CUDA(cudaGetLastError());
+  ++s->launches;
+  return SGDT_OK;
+}
+
+int sgdt_factor_merge_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  if (mode < 0 || mode >= s->order) return fail(SGDT_ERR_DOMAIN, "factor_merge_p2p: mode out of range");
+  TRY(check_factor_hyper(h));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (h->lr == 0.0) return SGDT_OK;
+  // the cut row this rank publishes: an exported row inside [row_lo, row_hi)
+  // (the row cut by the slice end; a row cut at the start belongs to the
+  // rank where it starts, one cut at both ends likewise)
+  const ShardPlan& sp = s->mode[mode].shard;
+  uint32_t own[2], k = 0;
+  for (uint32_t i = 0; i < sp.n_export; ++i)
+    if (sp.export_rows[i] >= sp.row_lo && sp.export_rows[i] < sp.row_hi) own[k++] = sp.export_rows[i];
+  if (k == 0) return SGDT_OK;
+  merge_records_kernel<<<1, 128, 0, s->stream>>>(s->xrec, s->world, s->rec_stride, s->RP, k, own[0],
+                                                 k > 1 ? own[1] : 0, s->merge_rows, s->merge_g);
+  SGDT_CUDA(cudaGetLastError());
+  ++s->launches;
+  return launch_factor_finish(*s, mode, *h, k, s->merge_rows, s->merge_g);
+}
+
+int sgdt_check(sgdt_session* s) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  SGDT_CUDA(cudaStreamSynchronize(s->side));
+  return sync_and_flag(*s);
 }
 
 int sgdt_synchronize(sgdt_session* s) {

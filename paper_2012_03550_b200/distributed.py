@@ -90,6 +90,11 @@ class ThreadGroup(Group):
     def barrier(self):
         self.s.bar.wait()
 
+    def stream_barrier(self, sess) -> None:
+        """Order every rank's queued device work before any rank's next work."""
+        sess.synchronize()
+        self.s.bar.wait()
+
 
 class TorchGroup(Group):
     """torch.distributed process group (NCCL for GPU ranks, gloo on CPU)."""
@@ -120,6 +125,25 @@ class TorchGroup(Group):
     def barrier(self):
         self.dist.barrier()
 
+    def stream_barrier(self, sess) -> None:
+        """NCCL: a one-element all-reduce enqueued on the session's stream --
+        it completes on a rank only after every rank's earlier kernels (and
+        their peer stores) completed, with no host synchronisation.  gloo:
+        synchronise, then a host barrier."""
+        if not self.nccl:
+            sess.synchronize()
+            self.dist.barrier()
+            return
+        torch = self.torch
+        if not hasattr(self, "_tok"):
+            self._tok = torch.zeros(1, device=self.device)
+            self._streams = {}
+        st = self._streams.get(sess.stream)
+        if st is None:
+            st = self._streams[sess.stream] = torch.cuda.ExternalStream(sess.stream)
+        with torch.cuda.stream(st):
+            self.dist.all_reduce(self._tok)
+
 
 # ----------------------------------------------------------------------------
 # the sharded GPU session
@@ -146,6 +170,15 @@ def _bind():
     L.sgdt_factor_device_ptr.argtypes = [vp, C.c_int, C.POINTER(C.c_void_p)]
     L.sgdt_refresh_q.argtypes = [vp, C.c_int]
     L.sgdt_synchronize.argtypes = [vp]
+    L.sgdt_peer_buffers.argtypes = [vp, C.POINTER(vp)]
+    L.sgdt_peer_ipc_handles.argtypes = [vp, vp]
+    L.sgdt_ipc_open.argtypes = [vp, C.c_int, C.POINTER(vp)]
+    L.sgdt_set_peers.argtypes = [vp, C.POINTER(vp)]
+    L.sgdt_core_epoch_async.argtypes = [vp, C.POINTER(sgdt.CoreHyper)]
+    L.sgdt_sample_ahead.argtypes = [vp, C.POINTER(sgdt.CoreHyper)]
+    L.sgdt_factor_mode_p2p.argtypes = [vp, C.c_int, C.POINTER(sgdt.FactorHyper)]
+    L.sgdt_factor_merge_p2p.argtypes = [vp, C.c_int, C.POINTER(sgdt.FactorHyper)]
+    L.sgdt_check.argtypes = [vp]
     L._shard_bound = True
     return L
 
@@ -173,6 +206,7 @@ class ShardedSession(sgdt.Session):
         self.R = int(R)
         self.nnz = len(self._tr.values)
         self.rank, self.world = rank, world
+        self.device = device
         h = C.c_void_p()
         sgdt._ck(L.sgdt_session_create_shard(C.byref(self._tr.desc), C.byref(self._te.desc) if self._te else None,
                                              sgdt._p(self.J, C.c_uint32), self.R, device, rank, world, C.byref(h)))
@@ -219,6 +253,43 @@ class ShardedSession(sgdt.Session):
 
     def synchronize(self) -> None:
         sgdt._ck(_bind().sgdt_synchronize(self.h))
+
+    # ---- peer-memory publication (NVLink P2P) ------------------------------
+    @property
+    def n_peer_buffers(self) -> int:
+        return 2 * self.order + 1
+
+    def peer_buffers(self) -> list[int]:
+        out = (C.c_void_p * self.n_peer_buffers)()
+        sgdt._ck(_bind().sgdt_peer_buffers(self.h, out))
+        return [int(p or 0) for p in out]
+
+    def peer_ipc_handles(self) -> np.ndarray:
+        out = np.zeros(self.n_peer_buffers * 64, np.uint8)
+        sgdt._ck(_bind().sgdt_peer_ipc_handles(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def set_peers(self, table) -> None:
+        """table: world x (2N+1) device pointers valid in this process."""
+        flat = [int(p) for row in table for p in row]
+        arr = (C.c_void_p * len(flat))(*flat)
+        sgdt._ck(_bind().sgdt_set_peers(self.h, arr))
+        self.peers_set = True
+
+    def core_epoch_async(self, ch: sgdt.CoreHyper) -> None:
+        sgdt._ck(_bind().sgdt_core_epoch_async(self.h, C.byref(ch)))
+
+    def sample_ahead(self, ch: sgdt.CoreHyper) -> None:
+        sgdt._ck(_bind().sgdt_sample_ahead(self.h, C.byref(ch)))
+
+    def factor_mode_p2p(self, n: int, fh: sgdt.FactorHyper) -> None:
+        sgdt._ck(_bind().sgdt_factor_mode_p2p(self.h, n, C.byref(fh)))
+
+    def factor_merge_p2p(self, n: int, fh: sgdt.FactorHyper) -> None:
+        sgdt._ck(_bind().sgdt_factor_merge_p2p(self.h, n, C.byref(fh)))
+
+    def check(self) -> None:
+        sgdt._ck(_bind().sgdt_check(self.h))
 
 
 # ----------------------------------------------------------------------------
@@ -288,3 +359,62 @@ def run_epochs_sharded(sess, group: Group, ch, fh, epochs: int = 1) -> None:
     for _ in range(epochs):
         sess.core_epoch(ch.lr, ch.reg, ch.batch_m, bool(ch.resample_per_mode), bool(ch.incremental_residual))
         factor_epoch_sharded(sess, group, fh)
+
+
+# ----------------------------------------------------------------------------
+# peer-memory publication: the finaliser's stores are the all-gather
+# ----------------------------------------------------------------------------
+def connect_peers(sess, group: Group) -> None:
+    """Give every rank the other ranks' A^(n)/Q^(n)/record buffers.  Ranks in
+    one process (ThreadGroup) exchange raw device pointers; ranks in separate
+    processes exchange CUDA IPC handles and map them (sgdt_ipc_open)."""
+    if isinstance(group, ThreadGroup):
+        table = group.all_gather(np.array(sess.peer_buffers(), np.uint64))
+        sess.set_peers([[int(p) for p in row] for row in table])
+        return
+    L = _bind()
+    handles = group.all_gather(sess.peer_ipc_handles())
+    own = sess.peer_buffers()
+    dev = sess.device if hasattr(sess, "device") else -1
+    table = []
+    for r, hs in enumerate(handles):
+        if r == group.rank:
+            table.append(own)
+            continue
+        row = []
+        for i in range(sess.n_peer_buffers):
+            p = C.c_void_p()
+            h = np.ascontiguousarray(hs[i * 64:(i + 1) * 64], np.uint8)
+            sgdt._ck(L.sgdt_ipc_open(h.ctypes.data_as(C.c_void_p), dev, C.byref(p)))
+            row.append(int(p.value))
+        table.append(row)
+    sess.set_peers(table)
+
+
+def factor_epoch_p2p(sess, group: Group, fh) -> None:
+    """update_factor_epoch over P ranks with peer-memory publication: per
+    mode, the local pass (every finalised row stored into every rank's A^(n)
+    and Q^(n), the cut rows' partials into every rank's record slot), a
+    barrier, the owner's merge + finalisation of its cut row (stored
+    everywhere), a barrier.  No host round trip, no broadcast, no Q refresh.
+    The leading barrier orders the peers' stores after every rank's core
+    phase, which reads every A^(k) row and rewrites every Q^(k) row."""
+    group.stream_barrier(sess)
+    for n in range(sess.order):
+        sess.factor_mode_p2p(n, fh)
+        group.stream_barrier(sess)
+        sess.factor_merge_p2p(n, fh)
+        group.stream_barrier(sess)
+
+
+def run_epochs_p2p(sess, group: Group, ch, fh, epochs: int = 1) -> None:
+    """`epochs` x (replicated core phase; peer-published sharded factor
+    phase), one host synchronisation (the numeric check) at the end."""
+    if not getattr(sess, "peers_set", False):
+        connect_peers(sess, group)
+    for e in range(epochs):
+        sess.core_epoch_async(ch)
+        if e + 1 < epochs:  # next epoch's Psi on the side stream, under this factor phase
+            sess.sample_ahead(ch)
+        factor_epoch_p2p(sess, group, fh)
+    sess.check()

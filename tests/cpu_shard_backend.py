@@ -109,3 +109,53 @@ class CpuShard:
 
     def refresh_q(self, n):
         pass  # Q is recomputed from A on demand
+
+    # -- peer-memory publication (emulated: peers are in-process objects) ---
+    _registry: dict = {}
+
+    @property
+    def n_peer_buffers(self):
+        return 2 * self.order + 1
+
+    def peer_buffers(self):
+        tok = id(self)
+        CpuShard._registry[tok] = self
+        return [tok] * self.n_peer_buffers
+
+    def set_peers(self, table):
+        self.peers = [CpuShard._registry[int(row[0])] for r, row in enumerate(table) if r != self.rank]
+        self.rec = {}
+        self.peers_set = True
+
+    def synchronize(self):
+        pass
+
+    def _publish_row(self, n, row):
+        for p in self.peers:
+            p.A[n][row] = self.A[n][row]
+
+    def factor_mode_p2p(self, n, fh):
+        rows, g = self.factor_mode_local(n, fh)
+        info = self.shard_info(n)
+        qb, qe = self.slices[n]
+        if qb < qe:  # every row this rank finalised locally, published
+            ids = self.perm[n][qb:qe]
+            for row in np.unique(self.coords[ids, n]):
+                if int(row) not in list(info.export_rows[: info.n_export]):
+                    self._publish_row(n, int(row))
+        record = (list(int(r) for r in rows), [np.array(x) for x in g])
+        for dst in [self] + self.peers:
+            dst.rec[self.rank] = record
+
+    def factor_merge_p2p(self, n, fh):
+        info = self.shard_info(n)
+        own = [int(r) for r in info.export_rows[: info.n_export] if info.row_lo <= r < info.row_hi]
+        for row in own:
+            g = None
+            for w in range(self.world):
+                rows, gs = self.rec.get(w, ([], []))
+                for r, gg in zip(rows, gs):
+                    if r == row:
+                        g = gg.copy() if g is None else g + gg
+            self._finalize(n, row, g, fh)
+            self._publish_row(n, row)

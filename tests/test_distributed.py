@@ -83,6 +83,41 @@ def test_thread_ranks_match_single_rank_and_oracle(world):
             assert np.max(np.abs(s.A[n] - one.A[n])) <= 1e-12
 
 
+def run_threads_p2p(c, v, A, B, world):
+    groups = D.ThreadGroup.make(world)
+    sess = [CpuShard(DIMS, c, v, J, R, r, world, A, B) for r in range(world)]
+    errs = []
+
+    def body(r):
+        try:
+            D.connect_peers(sess[r], groups[r])
+            groups[r].barrier()
+            D.factor_epoch_p2p(sess[r], groups[r], FH)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            raise
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    return sess
+
+
+@pytest.mark.parametrize("world", [2, 3, 7, 16])
+def test_thread_ranks_peer_publication_matches_broadcast_path(world):
+    """The peer-store driver (records into every rank's slot, owner-only
+    finalisation of cut rows, rows stored straight into the peers) gives
+    exactly the broadcast driver's result on every rank."""
+    c, v, (A, B) = data()
+    want = run_threads(c, v, A, B, world)[0]
+    for s in run_threads_p2p(c, v, A, B, world):
+        for n in range(3):
+            assert np.array_equal(s.A[n], want.A[n])
+
+
 def _gloo_worker(rank, world, port, out_dir):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -150,6 +185,50 @@ def test_gpu_sharded_sessions_match_single_session(world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_peer_publication_matches_broadcast_path(world):
+    """Sharded sessions publishing through peer stores (ranks as threads on one
+    GPU: the peers' buffers are plain device pointers of the same process)
+    give exactly the host-merge + broadcast driver's model on every rank."""
+    from paper_2012_03550_b200 import sgdt
+    c, v, (A, B) = data(nnz=6000, seed=9)
+    A = [a.astype(np.float32).astype(np.float64) for a in A]
+    B = [b.astype(np.float32).astype(np.float64) for b in B]
+    fh = sgdt.FactorHyper(FH.lr, FH.reg, 1.0)
+    ch = sgdt.CoreHyper(0.01, 0.01, 256, 0, 0)
+    results = {}
+    for mode in ("broadcast", "p2p"):
+        groups = D.ThreadGroup.make(world)
+        sess = [D.ShardedSession(DIMS, c, v, J, R, r, world) for r in range(world)]
+        for s in sess:
+            s.set_model(A, B)
+            s.seed(4)
+        errs = []
+
+        def body(r):
+            try:
+                if mode == "p2p":
+                    D.run_epochs_p2p(sess[r], groups[r], ch, fh, 2)
+                else:
+                    D.run_epochs_sharded(sess[r], groups[r], ch, fh, 2)
+            except Exception as e:
+                errs.append(e)
+                raise
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errs, errs
+        results[mode] = [s.get_model() for s in sess]
+    for r in range(world):
+        for n in range(3):
+            assert np.array_equal(results["p2p"][r][0][n], results["broadcast"][0][0][n])
+            assert np.array_equal(results["p2p"][r][1][n], results["broadcast"][0][1][n])
+
+
+@pytest.mark.gpu
 def test_gpu_nccl_path_single_rank():
     """The NCCL publication path (torch tensor aliasing the session's A^(n),
     dist.broadcast on it) at world size 1."""
@@ -182,5 +261,13 @@ def test_gpu_nccl_path_single_rank():
         GA, GB = s.get_model()
         for n in range(3):
             assert np.array_equal(GA[n], SA[n]) and np.array_equal(GB[n], SB[n])
+        # the peer-store driver over the NCCL stream barrier (no peers at P = 1)
+        p = D.ShardedSession(DIMS, c, v, J, R, 0, 1)
+        p.set_model(A, B)
+        p.seed(4)
+        D.run_epochs_p2p(p, g, ch, fh, 2)
+        PA, PB = p.get_model()
+        for n in range(3):
+            assert np.array_equal(PA[n], SA[n]) and np.array_equal(PB[n], SB[n])
     finally:
         dist.destroy_process_group()

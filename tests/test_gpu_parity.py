@@ -333,6 +333,45 @@ def test_run_epochs_host_matches_set_run_get(factor_lr):
             assert np.array_equal(res[0][n], want[0][n]) and np.array_equal(res[1][n], want[1][n])
 
 
+def test_sample_ahead_matches_run_epochs_and_guards_the_rng():
+    """sgdt_sample_ahead + sgdt_core_epoch_async (the sharded driver's
+    overlapped sampler) give exactly run_epochs' model, RNG state and last
+    Psi; a pending draw refuses other RNG consumers and a setter discards it."""
+    from paper_2012_03550_b200 import distributed as D
+    dims, J, R = (40, 30, 20), (5, 5, 5), 5
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, R, 5000, 21, tm=0.0, ts=sig)
+    m = oracle_model(dims, J, R, 9, sd=sig, mean=0.0)
+    ch, fh = sg().CoreHyper(0.01, 0.01, 512, 0, 0), sg().FactorHyper(0.01, 0.01, 1.0)
+    a = session_for(dims, tr, J, R)
+    a.set_model(*m.params())
+    a.seed(3)
+    a.run_epochs(ch, fh, 3)
+    b = D.ShardedSession(dims, *tr, J, R, 0, 1)
+    b.set_model(*m.params())
+    b.seed(3)
+    for e in range(3):
+        b.core_epoch_async(ch)
+        if e < 2:
+            b.sample_ahead(ch)
+        b.factor_epoch(fh.lr, fh.reg, 1.0)
+    b.check()
+    for x, y in zip(a.get_model(), b.get_model()):
+        for n in range(3):
+            assert np.array_equal(x[n], y[n])
+    assert np.array_equal(a.last_batch(), b.last_batch())
+    sa, pa = a.get_rng()
+    sb, pb = b.get_rng()
+    assert pa == pb and np.array_equal(sa, sb)
+    b.sample_ahead(ch)
+    with pytest.raises(sg().ConfigError):
+        b.sample_batch(10)
+    with pytest.raises(sg().ConfigError):
+        b.run_epochs(ch, fh, 1)
+    b.seed(3)  # discards the pending draw
+    b.sample_batch(10)
+
+
 def test_run_epochs_pipelined_sampler_matches_oracle():
     """sgdt_run_epochs draws epoch e+1's Psi on a side stream during epoch e's
     factor phase; the RNG stream, the pool and every Psi must still be exactly
