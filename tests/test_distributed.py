@@ -228,6 +228,58 @@ def test_gpu_peer_publication_matches_broadcast_path(world):
             assert np.array_equal(results["p2p"][r][1][n], results["broadcast"][0][1][n])
 
 
+def _ipc_worker(rank, world, port, out_dir):
+    """One process per rank on the same GPU: peers mapped through CUDA IPC
+    handles, host (gloo) barriers -- no kernel waits on another rank."""
+    import torch
+    import torch.distributed as dist
+    from paper_2012_03550_b200 import sgdt
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c, v, (A, B) = data(nnz=6000, seed=9)
+    A = [a.astype(np.float32).astype(np.float64) for a in A]
+    B = [b.astype(np.float32).astype(np.float64) for b in B]
+    s = D.ShardedSession(DIMS, c, v, J, R, rank, world, device=0)
+    s.set_model(A, B)
+    s.seed(4)
+    D.run_epochs_p2p(s, D.TorchGroup(), sgdt.CoreHyper(0.01, 0.01, 256, 0, 0), sgdt.FactorHyper(FH.lr, FH.reg, 1.0), 2)
+    GA, GB = s.get_model()
+    np.save(os.path.join(out_dir, f"P_{rank}.npy"), np.concatenate([x.ravel() for x in GA + GB]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_ipc_peer_publication_two_processes(tmp_path):
+    """The cross-process form of the peer-store driver (sgdt_peer_ipc_handles /
+    sgdt_ipc_open) gives the single-process result on both ranks."""
+    from paper_2012_03550_b200 import sgdt
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.spawn(_ipc_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    c, v, (A, B) = data(nnz=6000, seed=9)
+    A = [a.astype(np.float32).astype(np.float64) for a in A]
+    B = [b.astype(np.float32).astype(np.float64) for b in B]
+    groups = D.ThreadGroup.make(2)
+    sess = [D.ShardedSession(DIMS, c, v, J, R, r, 2) for r in range(2)]
+    for x in sess:
+        x.set_model(A, B)
+        x.seed(4)
+    th = [threading.Thread(target=D.run_epochs_sharded,
+                           args=(sess[r], groups[r], sgdt.CoreHyper(0.01, 0.01, 256, 0, 0),
+                                 sgdt.FactorHyper(FH.lr, FH.reg, 1.0), 2)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    GA, GB = sess[0].get_model()
+    want = np.concatenate([x.ravel() for x in GA + GB])
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"P_{r}.npy"), want)
+
+
 @pytest.mark.gpu
 def test_gpu_nccl_path_single_rank():
     """The NCCL publication path (torch tensor aliasing the session's A^(n),
