@@ -144,7 +144,6 @@ def make_data(cfg: int, scale: float, device):
         spec=spec,
         train=(trc.cpu().numpy().astype(np.uint32), trv.cpu().numpy()),
         test=(tec.cpu().numpy().astype(np.uint32), tev.cpu().numpy()),
-        perms=[p.cpu().numpy().astype(np.uint32) for p in perms],
         gen_s=time.time() - t0,
     )
     del trc, trv, tec, tev, perms
@@ -268,7 +267,7 @@ def run_sharded(args, rank, world, local_rank):
     trc, trv = data["train"]
     nnz = len(trv)
     t0 = time.time()
-    s = D.ShardedSession(spec.dims, trc, trv, [J] * order, R, rank, world, test=data["test"], perms=data["perms"],
+    s = D.ShardedSession(spec.dims, trc, trv, [J] * order, R, rank, world, test=data["test"],
                          device=local_rank)
     setup_s = time.time() - t0
     A, B = init_model(spec.dims, J, R, *init_stats(cfg, spec), HYPER["seed"])
@@ -364,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
     nnz = len(trv)
 
     t0 = time.time()
-    s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"], perms=data["perms"],
+    s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"],
                      device=local_rank)
     setup_s = time.time() - t0
     A, B = init_model(spec.dims, J, R, *init_stats(cfg, spec), HYPER["seed"])

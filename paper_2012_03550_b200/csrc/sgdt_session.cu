@@ -125,30 +125,23 @@ int validate_desc(const sgdt_tensor_desc* d, const char* what) {
     return fail(SGDT_ERR_DATA, std::string(what) + ": entry count exceeds the 32-bit id space");
   for (int k = 0; k < d->order; ++k)
     if (d->dims[k] < 1) return fail(SGDT_ERR_DOMAIN, std::string(what) + ": every dim must be >= 1");
-  const int order = d->order;
-  for (uint64_t e = 0; e < d->nnz; ++e)
-    for (int k = 0; k < order; ++k) {
-      const uint32_t c = d->coords[e * order + k];
-      if (c < 1 || c > d->dims[k])
-        return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(e) +
-                                       ": coordinate out of range");
-    }
+  // coordinate ranges are checked on the device after the upload (check_coords)
   return SGDT_OK;
 }
 
 // Row offsets of mode n (CooTensor::mode_offsets, sptensor.cpp:107-111) and,
 // when no permutation is supplied, the stable counting sort itself.
 void host_mode_layout(const sgdt_tensor_desc* d, int n, std::vector<uint64_t>& off,
-                      std::vector<uint32_t>& perm) {
+                      std::vector<uint32_t>* perm) {
   const uint32_t dim = d->dims[n];
   const int order = d->order;
   off.assign(static_cast<size_t>(dim) + 1, 0);
   for (uint64_t e = 0; e < d->nnz; ++e) off[d->coords[e * order + n]]++;
   for (size_t i = 1; i <= dim; ++i) off[i] += off[i - 1];
-  if (d->mode_perm && d->mode_perm[n]) return;
-  perm.resize(d->nnz);
+  if (!perm) return;
+  perm->resize(d->nnz);
   std::vector<uint64_t> cursor(off.begin(), off.end() - 1);
-  for (uint64_t e = 0; e < d->nnz; ++e) perm[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
+  for (uint64_t e = 0; e < d->nnz; ++e) (*perm)[cursor[d->coords[e * order + n] - 1]++] = static_cast<uint32_t>(e);
 }
 
 // Rows shorter than this are processed one row per lane / lane group
@@ -245,50 +238,130 @@ __global__ void row_key_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, c
        q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t e = perm[q];
     keys[q] = (static_cast<uint64_t>(idx[static_cast<uint64_t>(n) * nnz + e]) << 32) |
-              idx[static_cast<uint64_t>(m) * nnz + e];
+              (m >= 0 ? idx[static_cast<uint64_t>(m) * nnz + e] : 0u);
   }
 }
 
-// Re-sorts d_perm[0, len) (a contiguous slice of the mode-n order) by
-// (i_n, i_m); the row grouping and row offsets are unchanged.
-int order_rows_by_secondary(Session& s, int n, uint32_t* d_perm, uint64_t len) {
+__global__ void iota_u32_kernel(uint32_t* p, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<uint32_t>(i);
+}
+
+// off[r] = first position of row r in the key-sorted order, off[dim] = len
+// (CooTensor::mode_offsets, sptensor.cpp:107-111), from the sorted keys.
+__global__ void row_offsets_kernel(const uint64_t* __restrict__ keys, uint64_t len, uint32_t dim,
+                                   uint64_t* __restrict__ off) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q <= len;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cur = q < len ? static_cast<int64_t>(keys[q] >> 32) : static_cast<int64_t>(dim);
+    const int64_t prev = q > 0 ? static_cast<int64_t>(keys[q - 1] >> 32) : -1;
+    for (int64_t r = prev + 1; r <= cur; ++r) off[r] = q;
+  }
+}
+
+struct DimList {
+  uint32_t d[kMaxOrder];
+};
+// Coordinate ranges of an uploaded record copy (idx = coord - 1, so 0 wraps
+// past every bound): the smallest offending entry id, or ~0.
+__global__ void check_coords_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, int order, DimList dims,
+                                    unsigned long long* first_bad) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    for (int k = 0; k < order; ++k)
+      if (idx[static_cast<uint64_t>(k) * nnz + e] >= dims.d[k]) atomicMin(first_bad, static_cast<unsigned long long>(e));
+}
+
+int check_coords(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, const char* what) {
+  DimList dl{};
+  for (int k = 0; k < d->order; ++k) dl.d[k] = d->dims[k];
+  unsigned long long* bad = nullptr;
+  TRY(dalloc(&bad, 1));
+  unsigned long long h = ~0ull;
+  int rc_ = SGDT_OK;
+  if (cudaMemcpyAsync(bad, &h, sizeof h, cudaMemcpyHostToDevice, s.stream) != cudaSuccess) rc_ = SGDT_ERR_INTERNAL;
+  if (rc_ == SGDT_OK) {
+    check_coords_kernel<<<grid_for(rc.nnz, s.num_sms), 256, 0, s.stream>>>(rc.idx, rc.nnz, d->order, dl, bad);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, s.stream) != cudaSuccess ||
+        cudaStreamSynchronize(s.stream) != cudaSuccess)
+      rc_ = SGDT_ERR_INTERNAL;
+  }
+  cudaFree(bad);
+  if (rc_ != SGDT_OK) {
+    cudaGetLastError();
+    return fail(SGDT_ERR_INTERNAL, std::string(what) + ": coordinate check failed");
+  }
+  if (h != ~0ull)
+    return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(h) + ": coordinate out of range");
+  return SGDT_OK;
+}
+
+// The whole mode-n order and its row offsets on the device (CooTensor::
+// mode_perm / mode_offsets, sptensor.cpp:102-117, built by a stable radix sort
+// instead of the host counting sort): rows ascending by i_n; inside a row by
+// the secondary mode's coordinate, ties in the given order.  host_perm: the
+// caller's bucket order (or null: entry order).  off (host) receives the
+// I_n + 1 offsets.  SGDT_ERR_CONFIG: nnz exceeds the sort's 31-bit item count
+// (the caller falls back to the host counting sort).
+int build_mode_order(Session& s, int n, const uint32_t* host_perm, uint32_t* d_perm, std::vector<uint64_t>& off) {
+  const uint64_t len = s.nnz;
+  if (len > static_cast<uint64_t>(INT_MAX)) return SGDT_ERR_CONFIG;
   const int m = secondary_mode(s, n);
-  if (m < 0 || len < 2 || len > static_cast<uint64_t>(INT_MAX)) return SGDT_OK;
-  uint64_t *k_in = nullptr, *k_out = nullptr;
+  if (host_perm) {
+    SGDT_CUDA(cudaMemcpyAsync(d_perm, host_perm, len * sizeof(uint32_t), cudaMemcpyHostToDevice, s.stream));
+  } else {
+    iota_u32_kernel<<<grid_for(len, s.num_sms), 256, 0, s.stream>>>(d_perm, len);
+    SGDT_CUDA(cudaGetLastError());
+  }
+  const bool sort = !(host_perm && m < 0);  // a given bucket order needs no sort without a secondary key
+  uint64_t *k_in = nullptr, *k_out = nullptr, *d_off = nullptr;
   uint32_t* p_out = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   int end_bit = 32;
   while (end_bit < 64 && (1ull << (end_bit - 32)) < s.dims[n]) ++end_bit;
+  const int begin_bit = m >= 0 ? 0 : 32;
   int rc = SGDT_OK;
-  auto release = [&] {
-    if (k_in) cudaFree(k_in);
-    if (k_out) cudaFree(k_out);
-    if (p_out) cudaFree(p_out);
-    if (tmp) cudaFree(tmp);
-  };
+  off.assign(static_cast<size_t>(s.dims[n]) + 1, 0);
   do {
     if ((rc = dalloc(&k_in, len)) != SGDT_OK) break;
-    if ((rc = dalloc(&k_out, len)) != SGDT_OK) break;
-    if ((rc = dalloc(&p_out, len)) != SGDT_OK) break;
+    if ((rc = dalloc(&d_off, off.size())) != SGDT_OK) break;
     row_key_kernel<<<grid_for(len, s.num_sms), 256, 0, s.stream>>>(s.train_rec.idx, s.nnz, d_perm, len, n, m,
                                                                     k_in);
     if (cudaGetLastError() != cudaSuccess) {
       rc = fail(SGDT_ERR_INTERNAL, "row_key_kernel launch failed");
       break;
     }
-    if (cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len), 0,
-                                        end_bit, s.stream) != cudaSuccess ||
-        cudaMalloc(&tmp, tmp_bytes) != cudaSuccess ||
-        cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len), 0,
-                                        end_bit, s.stream) != cudaSuccess ||
-        cudaMemcpyAsync(d_perm, p_out, len * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s.stream) != cudaSuccess ||
+    const uint64_t* keys = k_in;
+    if (sort && len > 1) {
+      if ((rc = dalloc(&k_out, len)) != SGDT_OK) break;
+      if ((rc = dalloc(&p_out, len)) != SGDT_OK) break;
+      if (cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len),
+                                          begin_bit, end_bit, s.stream) != cudaSuccess ||
+          cudaMalloc(&tmp, tmp_bytes) != cudaSuccess ||
+          cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, d_perm, p_out, static_cast<int>(len),
+                                          begin_bit, end_bit, s.stream) != cudaSuccess ||
+          cudaMemcpyAsync(d_perm, p_out, len * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s.stream) !=
+              cudaSuccess) {
+        cudaGetLastError();
+        rc = fail(SGDT_ERR_INTERNAL, "mode order (radix sort) failed");
+        break;
+      }
+      keys = k_out;
+    }
+    row_offsets_kernel<<<grid_for(len + 1, s.num_sms), 256, 0, s.stream>>>(keys, len, s.dims[n], d_off);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(off.data(), d_off, off.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s.stream) !=
+            cudaSuccess ||
         cudaStreamSynchronize(s.stream) != cudaSuccess) {
       cudaGetLastError();
-      rc = fail(SGDT_ERR_INTERNAL, "intra-row ordering (radix sort) failed");
+      rc = fail(SGDT_ERR_INTERNAL, "mode offsets failed");
     }
   } while (false);
-  release();
+  for (void* p : {(void*)k_in, (void*)k_out, (void*)d_off, (void*)p_out, tmp})
+    if (p) cudaFree(p);
   return rc;
 }
 
@@ -715,6 +788,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     }
     // records: entry order (kept for Psi gathers + train RMSE) and per mode
     TRY(upload_record_copy(*s, train, s->train_rec, nullptr, nullptr));
+    TRY(check_coords(*s, s->train_rec, train, "train"));
     uint32_t max_pieces = 0;
     std::vector<uint64_t> off;
     std::vector<uint32_t> perm;
@@ -722,8 +796,18 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     TRY(dalloc(&d_perm, s->nnz));
     for (int n = 0; n < s->order; ++n) {
       ModePlan& mp = s->mode[n];
-      host_mode_layout(train, n, off, perm);
-      const uint32_t* hperm = (train->mode_perm && train->mode_perm[n]) ? train->mode_perm[n] : perm.data();
+      const uint32_t* given = (train->mode_perm && train->mode_perm[n]) ? train->mode_perm[n] : nullptr;
+      {
+        const int rc = build_mode_order(*s, n, given, d_perm, off);
+        if (rc == SGDT_ERR_CONFIG) {  // beyond the device sort's item count: host counting sort
+          host_mode_layout(train, n, off, given ? nullptr : &perm);
+          if (!given) given = perm.data();
+          SGDT_CUDA(cudaMemcpyAsync(d_perm, given, s->nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
+        } else if (rc != SGDT_OK) {
+          cudaFree(d_perm);
+          return rc;
+        }
+      }
       // this rank's slice of the mode-n order (partition_even, scheduler.cpp:34-46)
       uint64_t qb = 0, qe = 0;
       {
@@ -733,14 +817,12 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
         qe = pe[rank];
       }
       const uint64_t len = qe - qb;
-      if (len) SGDT_CUDA(cudaMemcpyAsync(d_perm, hperm + qb, len * sizeof(uint32_t), cudaMemcpyHostToDevice, s->stream));
-      TRY(order_rows_by_secondary(*s, n, d_perm, len));
       mp.rec.nnz = len;
       TRY(dalloc(&mp.rec.idx, len * s->order));
       TRY(dalloc(&mp.rec.val, len));
       if (len) {
         gather_mode_copy_kernel<<<grid_for(len, s->num_sms), 256, 0, s->stream>>>(
-            s->train_rec.idx, s->train_rec.val, d_perm, s->nnz, len, s->order, mp.rec.idx, mp.rec.val);
+            s->train_rec.idx, s->train_rec.val, d_perm + qb, s->nnz, len, s->order, mp.rec.idx, mp.rec.val);
         SGDT_CUDA(cudaGetLastError());
       }
       s->h_row_ptr[n] = off;
@@ -772,6 +854,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     if (test) {
       s->nnz_test = test->nnz;
       TRY(upload_record_copy(*s, test, s->test_rec, nullptr, nullptr));
+      TRY(check_coords(*s, s->test_rec, test, "test"));
     }
     // model
     uint64_t stage = 0;

@@ -144,9 +144,11 @@ def teacher(spec: SynthSpec, device):
     return A, B
 
 
-def generate(spec: SynthSpec, device="cuda"):
+def generate(spec: SynthSpec, device="cuda", with_perms: bool = False):
     """Returns (train, test), each (coords u32 [nnz,N] 1-based, values f64) as
-    torch tensors on `device`, plus the mode-sorted permutations of train."""
+    torch tensors on `device`, plus (with_perms) the mode-sorted permutations
+    of train (the session builds its own mode orders on the device, so
+    callers normally leave them out)."""
     device = torch.device(device)
     if math.prod(spec.dims) >= 2**62:
         idx = _draw_tuples_wide(dataclasses.replace(spec), device)
@@ -183,7 +185,9 @@ def generate(spec: SynthSpec, device="cuda"):
     train = (coords[tr], v[tr])
     test = (coords[te], v[te])
     del coords, v
-    perms = [torch.sort(train[0][:, n], stable=True).indices.to(torch.int32) for n in range(len(spec.dims))]
+    perms = None
+    if with_perms:
+        perms = [torch.sort(train[0][:, n], stable=True).indices.to(torch.int32) for n in range(len(spec.dims))]
     return train, test, perms
 
 

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def c2():
     import torch
     from paper_2012_03550_b200 import synth
-    (trc, trv), (tec, tev), perms = synth.generate(synth.CONFIGS[2], "cuda")
+    (trc, trv), (tec, tev), perms = synth.generate(synth.CONFIGS[2], "cuda", with_perms=True)
     out = dict(dims=synth.CONFIGS[2].dims, train=(trc.cpu().numpy().astype(np.uint32), trv.cpu().numpy()),
                test=(tec.cpu().numpy().astype(np.uint32), tev.cpu().numpy()),
                perms=[p.cpu().numpy().astype(np.uint32) for p in perms])
