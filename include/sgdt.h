@@ -262,6 +262,15 @@ int sgdt_factor_merge_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h)
 /* Synchronise and check the numeric flag (SGDT_ERR_NUMERIC on divergence). */
 int sgdt_check(sgdt_session* s);
 
+/* train_test_split (sptensor.cpp:217-254) on the device: the Fisher-Yates
+ * of the entry ids 0..nnz-1 with Rng(seed) (nnz-1 draws, bit-exact: the
+ * sampler's parallel swap-chain resolution), then both halves sorted
+ * ascending.  test_ids receives llround(fraction * nnz) ids, train_ids the
+ * rest (host buffers).  DomainError for a fraction outside (0,1) or a
+ * degenerate split, as the reference. */
+int sgdt_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, int device, uint32_t* test_ids,
+                   uint32_t* train_ids);
+
 /* Device next_below over an explicit MT state (test hook for the rejection
  * path, rng.hpp:20-25): draws n values with bounds[i] sequentially. */
 int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,

@@ -98,12 +98,10 @@ std::pair<CooTensor, CooTensor> train_test_split(const CooTensor& t, double test
   if (ntest == 0 || ntest == nnz)
     throw DomainError("train_test_split: degenerate split (|test|=" + std::to_string(ntest) + " of " +
                       std::to_string(nnz) + ")");
+  // the Fisher-Yates with Rng(seed) and the two sorts run on the device
+  // (sgdt_split_ids: the sampler's swap-chain resolution, bit-exact)
   std::vector<std::uint32_t> ids(nnz);
-  std::iota(ids.begin(), ids.end(), 0u);
-  Rng rng(seed);
-  for (std::size_t i = 0; i + 1 < nnz; ++i) std::swap(ids[i], ids[i + static_cast<std::size_t>(rng.next_below(nnz - i))]);
-  std::sort(ids.begin(), ids.begin() + static_cast<std::ptrdiff_t>(ntest));
-  std::sort(ids.begin() + static_cast<std::ptrdiff_t>(ntest), ids.end());
+  detail::check(sgdt_split_ids(nnz, test_fraction, seed, -1, ids.data(), ids.data() + ntest), "train_test_split");
   auto take = [&](std::size_t b, std::size_t e) {
     std::vector<std::uint32_t> c;
     std::vector<double> v;

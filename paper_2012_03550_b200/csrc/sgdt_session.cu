@@ -1481,6 +1481,68 @@ int sgdt_check(sgdt_session* s) {
   return sync_and_flag(*s);
 }
 
+int sgdt_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, int device, uint32_t* test_ids,
+                   uint32_t* train_ids) {
+  if (!(test_fraction > 0.0 && test_fraction < 1.0))
+    return fail(SGDT_ERR_DOMAIN, "train_test_split: fraction must lie in (0,1)");
+  const uint64_t ntest = static_cast<uint64_t>(std::llround(test_fraction * static_cast<double>(nnz)));
+  if (ntest == 0 || ntest == nnz)
+    return fail(SGDT_ERR_DOMAIN, "train_test_split: degenerate split (|test|=" + std::to_string(ntest) + " of " +
+                                     std::to_string(nnz) + ")");
+  if (nnz > 0xFFFFFFFFull || nnz > static_cast<uint64_t>(INT_MAX))
+    return fail(SGDT_ERR_CONFIG, "split_ids: more entries than the device split supports");
+  if ((ntest && !test_ids) || !train_ids) return fail(SGDT_ERR_DOMAIN, "split_ids: null output");
+  if (device >= 0) SGDT_CUDA(cudaSetDevice(device));
+  // a sampler-only session: pool = iota, Rng(seed), nnz-1 draws
+  Session t;
+  SGDT_CUDA(cudaGetDevice(&t.device));
+  cudaDeviceProp prop{};
+  SGDT_CUDA(cudaGetDeviceProperties(&prop, t.device));
+  t.num_sms = prop.multiProcessorCount;
+  t.nnz = nnz;
+  const uint64_t m = nnz - 1;
+  uint32_t *keys_out = nullptr, *batch = nullptr;
+  void* tmp = nullptr;
+  int rc = [&]() -> int {
+    SGDT_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+    TRY(dalloc(&t.mt, 313));
+    uint64_t mt[313];
+    mt_seed(mt, seed);
+    mt[312] = 312;
+    SGDT_CUDA(cudaMemcpyAsync(t.mt, mt, sizeof mt, cudaMemcpyHostToDevice, t.stream));
+    TRY(dalloc(&t.pool, nnz));
+    TRY(dalloc(&t.head, nnz));
+    SGDT_CUDA(cudaMemsetAsync(t.head, 0, nnz * sizeof(unsigned long long), t.stream));
+    for (uint32_t** p : {&t.draw_j, &t.link, &t.kprev, &t.lprev, &t.dval}) TRY(dalloc(p, m));
+    TRY(dalloc(&batch, m));
+    TRY(launch_sampler(t, m, batch, t.stream));  // the pool is now the shuffled id array
+    TRY(dalloc(&keys_out, nnz));
+    size_t b1 = 0, b2 = 0;
+    SGDT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, t.pool, keys_out, static_cast<int>(ntest), 0, 32,
+                                             t.stream));
+    SGDT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b2, t.pool + ntest, keys_out + ntest,
+                                             static_cast<int>(nnz - ntest), 0, 32, t.stream));
+    SGDT_CUDA(cudaMalloc(&tmp, std::max(b1, b2)));
+    SGDT_CUDA(cub::DeviceRadixSort::SortKeys(tmp, b1, t.pool, keys_out, static_cast<int>(ntest), 0, 32, t.stream));
+    SGDT_CUDA(cub::DeviceRadixSort::SortKeys(tmp, b2, t.pool + ntest, keys_out + ntest,
+                                             static_cast<int>(nnz - ntest), 0, 32, t.stream));
+    SGDT_CUDA(cudaMemcpyAsync(test_ids, keys_out, ntest * sizeof(uint32_t), cudaMemcpyDeviceToHost, t.stream));
+    SGDT_CUDA(cudaMemcpyAsync(train_ids, keys_out + ntest, (nnz - ntest) * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, t.stream));
+    SGDT_CUDA(cudaStreamSynchronize(t.stream));
+    return SGDT_OK;
+  }();
+  for (void* p : {(void*)t.mt, (void*)t.pool, (void*)t.head, (void*)t.draw_j, (void*)t.link, (void*)t.kprev,
+                  (void*)t.lprev, (void*)t.dval, (void*)batch, (void*)keys_out, tmp})
+    if (p) cudaFree(p);
+  t.mt = nullptr;
+  t.pool = t.draw_j = t.link = t.kprev = t.lprev = t.dval = nullptr;
+  t.head = nullptr;
+  if (t.stream) cudaStreamDestroy(t.stream);
+  t.stream = nullptr;
+  return rc;
+}
+
 int sgdt_synchronize(sgdt_session* s) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   SGDT_CUDA(cudaSetDevice(s->device));

@@ -127,6 +127,7 @@ def load(build_if_missing: bool = True):
     L.sgdt_launch_count.restype = C.c_uint64
     L.sgdt_rng_next_below.argtypes = [u64p, C.c_uint32, u64p, C.c_uint64, u64p, u64p, u32p]
     L.sgdt_partition_even.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p]
+    L.sgdt_split_ids.argtypes = [C.c_uint64, C.c_double, C.c_uint64, C.c_int, u32p, u32p]
     _lib = L
     return L
 
@@ -157,6 +158,17 @@ def partition_even(count: int, workers: int):
     e = np.empty(workers, np.uint64)
     _lib.sgdt_partition_even(count, workers, _p(b, C.c_uint64), _p(e, C.c_uint64))
     return list(zip(b.tolist(), e.tolist()))
+
+
+def split_ids(nnz: int, test_fraction: float, seed: int, device: int = -1):
+    """train_test_split's id halves (sptensor.cpp:217-254) on the device:
+    returns (test_ids, train_ids), each sorted ascending."""
+    load()
+    ntest = int(round(test_fraction * nnz)) if 0.0 < test_fraction < 1.0 else 0
+    te = np.empty(max(ntest, 1), np.uint32)
+    tr = np.empty(max(nnz - ntest, 1), np.uint32)
+    _ck(_lib.sgdt_split_ids(nnz, test_fraction, seed, device, _p(te, C.c_uint32), _p(tr, C.c_uint32)))
+    return te[:ntest], tr[: nnz - ntest]
 
 
 def rng_next_below(state: np.ndarray, pos: int, bounds: np.ndarray):

@@ -15,7 +15,9 @@ unit-variance teacher, built here with the same conventions:
     that xhat has unit variance (Var = R (J sigma^4)^N);
   * config 2 values: xhat affinely mapped to mean 3 / std 1, rounded to an
     integer and clipped to [1, 5] (ratings);  configs 3-5: xhat + N(0, noise^2).
-The 90/10 split draws a seeded permutation; each half is kept in entry order.
+The 90/10 split is the reference's train_test_split (Fisher-Yates with
+Rng(seed + 7), both halves in entry order), computed on the device by
+sgdt_split_ids.
 No dataset is fetched or reproduced: Netflix/MovieLens/Yahoo are not here.
 """
 from __future__ import annotations
@@ -23,6 +25,7 @@ from __future__ import annotations
 import dataclasses
 import math
 
+import numpy as np
 import torch
 
 
@@ -177,11 +180,14 @@ def generate(spec: SynthSpec, device="cuda", with_perms: bool = False):
     del xhat, Q
     coords = torch.stack([i.to(torch.int32) + 1 for i in idx], 1)
     del idx
-    ntest = int(round(spec.test_fraction * nnz))
-    perm = torch.randperm(nnz, generator=gen, device=device)
-    te = torch.sort(perm[:ntest]).values
-    tr = torch.sort(perm[ntest:]).values
-    del perm
+    # the reference's split (sptensor.cpp:217-254: Fisher-Yates with
+    # Rng(seed), both halves sorted), run on the device by sgdt_split_ids
+    from . import sgdt
+    te_ids, tr_ids = sgdt.split_ids(nnz, spec.test_fraction, spec.seed + 7,
+                                    device.index if device.type == "cuda" and device.index is not None else -1)
+    te = torch.from_numpy(te_ids.astype(np.int64)).to(device)
+    tr = torch.from_numpy(tr_ids.astype(np.int64)).to(device)
+    del te_ids, tr_ids
     train = (coords[tr], v[tr])
     test = (coords[te], v[te])
     del coords, v

@@ -372,6 +372,24 @@ def test_sample_ahead_matches_run_epochs_and_guards_the_rng():
     b.sample_batch(10)
 
 
+@pytest.mark.parametrize("nnz,frac,seed", [(2, 0.5, 1), (10, 0.3, 7), (5000, 0.1, 42), (1_000_003, 0.1, 2026)])
+def test_split_ids_bit_exact(nnz, frac, seed):
+    """sgdt_split_ids: the reference's full Fisher-Yates split on the device,
+    id for id (the oracle is pinned to the reference's train_test_split)."""
+    te, tr = sg().split_ids(nnz, frac, seed)
+    ids = np.empty(nnz, np.uint32)
+    nt = O.C.c_size_t()
+    O._ck(O.lib().or_train_test_split_ids(nnz, frac, seed, ids, O.C.byref(nt)), "split")
+    assert np.array_equal(te, ids[: nt.value]) and np.array_equal(tr, ids[nt.value:])
+
+
+def test_split_ids_errors():
+    with pytest.raises(sg().DomainError):
+        sg().split_ids(100, 0.0, 1)
+    with pytest.raises(sg().DomainError):
+        sg().split_ids(3, 0.01, 1)
+
+
 def test_run_epochs_pipelined_sampler_matches_oracle():
     """sgdt_run_epochs draws epoch e+1's Psi on a side stream during epoch e's
     factor phase; the RNG stream, the pool and every Psi must still be exactly
