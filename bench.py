@@ -409,13 +409,22 @@ def run_ours(args, rank, world, local_rank):
     avg_mode_ms = sum(mode_ms) / order
     achieved_gbs = nnz * bu / (avg_mode_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = None
+    traffic = l2_traffic = None
     tpath = os.path.join(ROOT, "profiles", "factor_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"config{cfg}")
+            tj = json.load(open(tpath))
+            traffic, l2_traffic = tj.get(f"config{cfg}"), tj.get(f"config{cfg}_l2")
         except Exception:
-            traffic = None
+            traffic = l2_traffic = None
+    # bytes outside B_u, per epoch: the mode-n row traffic of the
+    # factor phase (read a and Q^(n), write a and Q^(n) per non-empty row) and
+    # the Q^(k) refresh at the end of the core phase
+    rows_nonempty = [int(np.count_nonzero(np.bincount(trc[:, n], minlength=spec.dims[n] + 1)))
+                     for n in range(order)]
+    overhead = {"mode_rows": sum(4 * (2 * J + 2 * R) * r for r in rows_nonempty),
+                "q_refresh": sum(4 * d * (J + R) for d in spec.dims),
+                "b_u_total": units * bu}
 
     rmse = s.eval(1)[0]
 
@@ -474,9 +483,11 @@ def run_ours(args, rank, world, local_rank):
                        "test_rmse_after": rmse, "data_gen_s": data["gen_s"], "setup_s": setup_s},
             "phase_ms": {"core": timing.core_ms, "factor": timing.factor_ms, "factor_modes": mode_ms},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": achieved_gbs / peak, "traffic": traffic,
-                         "kernel": "factor_chunk_kernel + factor_split_kernel (one mode)",
-                         "bytes_per_unit": bu, "units_per_launch": nnz, "peak_source": peak_src},
+                         "frac": achieved_gbs / peak, "traffic": traffic, "l2_traffic": l2_traffic,
+                         "kernel": ("factor_chunk_kernel" if (R + 3) // 4 * 4 <= 12 else "factor_group_kernel")
+                                   + " + factor_split_kernel (one mode)",
+                         "bytes_per_unit": bu, "units_per_launch": nnz, "peak_source": peak_src,
+                         "overhead_bytes_per_epoch": overhead},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
