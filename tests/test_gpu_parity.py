@@ -164,6 +164,10 @@ CASES = [
     dict(dims=(300, 40, 30), J=(28, 28, 28), R=27, nnz=20000, batch_m=500),
     dict(dims=(9, 8, 7, 6), J=(16, 16, 16, 16), R=16, nnz=3000, batch_m=256),
     dict(dims=(9, 8, 7, 6, 5), J=(10, 10, 10, 10, 10), R=10, nnz=3000, batch_m=256),
+    # J > 32: the second column chunk of the core pass, the finaliser's and the
+    # tiled Q refresh's j loops (J not a multiple of 4 takes the scalar tile path)
+    dict(dims=(40, 30, 20), J=(64, 40, 37), R=32, nnz=6000, batch_m=700),
+    dict(dims=(60, 50, 40), J=(50, 33, 45), R=12, nnz=8000, batch_m=900),
 ]
 
 
