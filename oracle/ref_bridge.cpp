@@ -12,6 +12,9 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <span>
+#include <string>
+#include <cstdio>
 #include <vector>
 
 #include "sptucker/common.hpp"
@@ -363,6 +366,190 @@ int ref_time_epochs(void* train_t, const std::uint32_t* J, std::uint32_t R, doub
     std::sort(secs.begin(), secs.end());
     const std::size_t k = secs.size();
     *seconds = k % 2 ? secs[k / 2] : 0.5 * (secs[k / 2 - 1] + secs[k / 2]);
+  });
+}
+
+// ---- host I/O and the ratings generator (golden fixtures for the C++ host
+// API: tests/golden/make_io_golden.py).  Every call stores the exception text
+// for ref_last_message().
+thread_local std::string g_msg;
+
+#define GUARD_MSG(...)                                   \
+  try {                                                  \
+    g_msg.clear();                                       \
+    __VA_ARGS__;                                         \
+    return 0;                                            \
+  } catch (const std::exception& ex) {                   \
+    g_msg = ex.what();                                   \
+    return code_of(std::current_exception());            \
+  } catch (...) {                                        \
+    return code_of(std::current_exception());            \
+  }
+
+const char* ref_last_message() { return g_msg.c_str(); }
+
+// CooTensor::load_delimited (sptensor.cpp:120-195) into a new tensor handle.
+void* ref_tensor_load_delimited(const char* path, std::size_t order, int skip_header, int zero_replace,
+                                double zero_replacement, std::size_t n_override, const std::uint32_t* dims_override,
+                                int* rc) {
+  void* out = nullptr;
+  *rc = [&]() -> int {
+    GUARD_MSG({
+      LoadOptions o;
+      o.skip_header = skip_header != 0;
+      o.zero_policy = zero_replace ? ZeroPolicy::Replace : ZeroPolicy::Reject;
+      o.zero_replacement = zero_replacement;
+      o.dims_override.assign(dims_override, dims_override + n_override);
+      auto* h = new RefTensor;
+      h->t = std::make_unique<CooTensor>(CooTensor::load_delimited(path, order, o));
+      out = h;
+    });
+  }();
+  return out;
+}
+
+int ref_tensor_save_delimited(void* h, const char* path) {
+  GUARD_MSG({ static_cast<RefTensor*>(h)->t->save_delimited(path); });
+}
+
+// dims (order), nnz; coords/values may be null (query sizes first).
+int ref_tensor_get(void* h, std::uint32_t* dims, std::size_t* nnz, std::uint32_t* coords, double* values) {
+  GUARD_MSG({
+    const CooTensor& t = *static_cast<RefTensor*>(h)->t;
+    for (std::size_t k = 0; k < t.order(); ++k) dims[k] = t.shape().dim(k);
+    *nnz = t.nnz();
+    if (coords)
+      for (std::size_t e = 0; e < t.nnz(); ++e) {
+        const auto c = t.coord(e);
+        std::copy(c.begin(), c.end(), coords + e * t.order());
+      }
+    if (values) std::copy(t.values().begin(), t.values().end(), values);
+  });
+}
+
+int ref_model_save(void* h, const char* path) {
+  GUARD_MSG({ static_cast<RefModel*>(h)->m->save(path); });
+}
+
+// TuckerModel::load (model.cpp:232-280); order/dims/J/R of the loaded model
+// are written to the out-params (dims, J sized 64).
+void* ref_model_load(const char* path, int* order, std::uint32_t* dims, std::uint32_t* J, std::uint32_t* R,
+                     int* rc) {
+  void* out = nullptr;
+  *rc = [&]() -> int {
+    GUARD_MSG({
+      auto* h = new RefModel;
+      h->m = std::make_unique<TuckerModel>(TuckerModel::load(path));
+      *order = static_cast<int>(h->m->order());
+      for (std::size_t n = 0; n < h->m->order(); ++n) {
+        dims[n] = h->m->shape().dim(n);
+        J[n] = h->m->ranks().J[n];
+      }
+      *R = h->m->ranks().r_core;
+      out = h;
+    });
+  }();
+  return out;
+}
+
+// write_metrics_csv (eval.cpp:78-97); rows: n x 10 doubles in column order
+// (epoch, core_s, factor_s, total_s, train_rmse, train_mae, test_rmse,
+// test_mae, peak_bytes, comm_bytes); comments: '\n'-separated.
+int ref_write_metrics_csv(const char* path, std::size_t n, const double* rows, const char* comments) {
+  GUARD_MSG({
+    std::vector<EpochMetrics> r(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      const double* x = rows + i * 10;
+      r[i].epoch = static_cast<std::size_t>(x[0]);
+      r[i].core_s = x[1];
+      r[i].factor_s = x[2];
+      r[i].total_s = x[3];
+      r[i].train_rmse = x[4];
+      r[i].train_mae = x[5];
+      r[i].test_rmse = x[6];
+      r[i].test_mae = x[7];
+      r[i].peak_bytes = static_cast<std::uint64_t>(x[8]);
+      r[i].comm_bytes = static_cast<std::uint64_t>(x[9]);
+    }
+    std::vector<std::string> c;
+    std::string cur;
+    for (const char* p = comments; p && *p; ++p) {
+      if (*p == '\n') {
+        c.push_back(cur);
+        cur.clear();
+      } else {
+        cur += *p;
+      }
+    }
+    if (!cur.empty()) c.push_back(cur);
+    write_metrics_csv(path, r, c);
+  });
+}
+
+// parse_metrics_csv (eval.cpp:99-146): rows out as n x 10 doubles (capacity
+// max_rows), comments '\n'-joined into comments_out (capacity cap).
+int ref_parse_metrics_csv(const char* path, std::size_t max_rows, double* rows, std::size_t* n,
+                          char* comments_out, std::size_t cap) {
+  GUARD_MSG({
+    std::vector<std::string> c;
+    const auto r = parse_metrics_csv(path, &c);
+    *n = r.size();
+    for (std::size_t i = 0; i < r.size() && i < max_rows; ++i) {
+      double* x = rows + i * 10;
+      x[0] = static_cast<double>(r[i].epoch);
+      x[1] = r[i].core_s;
+      x[2] = r[i].factor_s;
+      x[3] = r[i].total_s;
+      x[4] = r[i].train_rmse;
+      x[5] = r[i].train_mae;
+      x[6] = r[i].test_rmse;
+      x[7] = r[i].test_mae;
+      x[8] = static_cast<double>(r[i].peak_bytes);
+      x[9] = static_cast<double>(r[i].comm_bytes);
+    }
+    std::string j;
+    for (const auto& s : c) j += s + "\n";
+    std::snprintf(comments_out, cap, "%s", j.c_str());
+  });
+}
+
+// synth_ratings (synth.cpp:83-103).
+int ref_synth_ratings(int order, const std::uint32_t* dims, const std::uint32_t* tJ, std::uint32_t tR,
+                      std::size_t nnz, double tmean, double tsd, std::uint64_t seed, double target_mean,
+                      double target_sd, double noise, int half_steps, double min_v, double max_v,
+                      std::uint32_t* coords_out, double* values_out) {
+  GUARD_MSG({
+    RatingSpec spec;
+    spec.base.shape = Shape(std::vector<std::uint32_t>(dims, dims + order));
+    spec.base.teacher_ranks = Ranks{std::vector<std::uint32_t>(tJ, tJ + order), tR};
+    spec.base.nnz = nnz;
+    spec.base.teacher_mean = tmean;
+    spec.base.teacher_stddev = tsd;
+    spec.base.seed = seed;
+    spec.target_mean = target_mean;
+    spec.target_stddev = target_sd;
+    spec.noise_stddev = noise;
+    spec.quantize_half_steps = half_steps != 0;
+    spec.min_value = min_v;
+    spec.max_value = max_v;
+    const CooTensor t = synth_ratings(spec);
+    for (std::size_t e = 0; e < t.nnz(); ++e) {
+      const auto c = t.coord(e);
+      std::copy(c.begin(), c.end(), coords_out + e * order);
+      values_out[e] = t.value(e);
+    }
+  });
+}
+
+// unfold_col_index / vec_index / invert_vec_index (sptensor.cpp:40-78).
+int ref_indexing(int order, const std::uint32_t* dims, const std::uint32_t* coord, std::size_t mode,
+                 std::uint64_t* col, std::uint64_t* vec, std::uint32_t* inv_coord) {
+  GUARD_MSG({
+    const Shape shape(std::vector<std::uint32_t>(dims, dims + order));
+    const std::span<const std::uint32_t> c(coord, static_cast<std::size_t>(order));
+    *col = unfold_col_index(shape, c, mode);
+    *vec = vec_index(shape, c, mode);
+    invert_vec_index(shape, *vec, mode, std::span<std::uint32_t>(inv_coord, static_cast<std::size_t>(order)));
   });
 }
 

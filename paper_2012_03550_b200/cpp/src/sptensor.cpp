@@ -30,22 +30,37 @@ Shape::Shape(std::vector<std::uint32_t> dims) : dims_(std::move(dims)) {
 
 namespace {
 
-// Duplicate detection: sort (128-bit) linear positions and look for equal
-// neighbours.  The linear key of the reference (mode 1 fastest) wraps for
-// shapes beyond 2^64 elements, hence the two-word key.
-bool has_duplicate(const Shape& shape, const std::vector<std::uint32_t>& coords, std::size_t nnz) {
+// Duplicate detection: sort (128-bit linear position, entry id) pairs.  The
+// reference reports the first entry, in entry order, whose position was seen
+// before (sptensor.cpp:90-99): in every group of equal positions that is the
+// group's second-smallest id, and the answer is the smallest of those (or nnz
+// when there is none).  The reference's 64-bit key wraps for shapes beyond
+// 2^64 elements, hence the two-word key.
+std::size_t first_duplicate(const Shape& shape, const std::vector<std::uint32_t>& coords, std::size_t nnz) {
   const std::size_t order = shape.order();
-  std::vector<std::pair<std::uint64_t, std::uint64_t>> keys(nnz);
+  struct Key {
+    std::uint64_t hi, lo;
+    std::uint32_t e;
+  };
+  std::vector<Key> keys(nnz);
   for (std::size_t e = 0; e < nnz; ++e) {
     unsigned __int128 key = 0, stride = 1;
     for (std::size_t k = 0; k < order; ++k) {
       key += static_cast<unsigned __int128>(coords[e * order + k] - 1) * stride;
       stride *= shape.dim(k);
     }
-    keys[e] = {static_cast<std::uint64_t>(key >> 64), static_cast<std::uint64_t>(key)};
+    keys[e] = {static_cast<std::uint64_t>(key >> 64), static_cast<std::uint64_t>(key), static_cast<std::uint32_t>(e)};
   }
-  std::sort(keys.begin(), keys.end());
-  return std::adjacent_find(keys.begin(), keys.end()) != keys.end();
+  std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+    return a.hi != b.hi ? a.hi < b.hi : a.lo != b.lo ? a.lo < b.lo : a.e < b.e;
+  });
+  std::size_t first = nnz;
+  for (std::size_t i = 1; i < nnz; ++i) {
+    const bool same = keys[i].hi == keys[i - 1].hi && keys[i].lo == keys[i - 1].lo;
+    const bool second_of_group = same && (i < 2 || keys[i - 2].hi != keys[i].hi || keys[i - 2].lo != keys[i].lo);
+    if (second_of_group) first = std::min<std::size_t>(first, keys[i].e);
+  }
+  return first;
 }
 
 }  // namespace
@@ -57,12 +72,21 @@ CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector
   if (nnz == 0) throw DataError("tensor has no entries");
   if (coords_.size() != nnz * order) throw DataError("coords/values length mismatch");
   if (nnz > std::numeric_limits<std::uint32_t>::max()) throw DataError("entry count exceeds the 32-bit id space");
-  for (std::size_t e = 0; e < nnz; ++e)
+  // The reference checks entry by entry, range before duplicate; the first
+  // failing entry decides the message.  Entries before the first out-of-range
+  // one are all in range, so a duplicate found below it is exact.
+  std::size_t bad_range = nnz;
+  for (std::size_t e = 0; e < nnz && bad_range == nnz; ++e)
     for (std::size_t k = 0; k < order; ++k) {
       const std::uint32_t c = coords_[e * order + k];
-      if (c < 1 || c > shape_.dim(k)) throw DataError("entry " + std::to_string(e) + ": coordinate out of range");
+      if (c < 1 || c > shape_.dim(k)) {
+        bad_range = e;
+        break;
+      }
     }
-  if (has_duplicate(shape_, coords_, nnz)) throw DataError("duplicate coordinate");
+  const std::size_t dup = first_duplicate(shape_, coords_, nnz);
+  if (dup < bad_range) throw DataError("entry " + std::to_string(dup) + ": duplicate coordinate");
+  if (bad_range < nnz) throw DataError("entry " + std::to_string(bad_range) + ": coordinate out of range");
 
   // Stable counting sort per mode: bucket i holds the entries with i_n = i in
   // ascending entry id (the order the device mode copies inherit).

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <filesystem>
 #include <functional>
 #include <numeric>
 #include <set>
@@ -20,7 +22,10 @@
 #include "sptucker/core_optimizer.hpp"
 #include "sptucker/eval.hpp"
 #include "sptucker/factor_optimizer.hpp"
+#include "sptucker/synth.hpp"
 #include "sptucker/trainer.hpp"
+
+#include <unistd.h>
 
 using namespace sptucker;
 
@@ -350,6 +355,234 @@ void test_config_errors() {
   CHECK(throws_as<ConfigError>([&] { train_from_scratch(t, nullptr, h); }));
 }
 
+// ---------------------------------------------------------------- I/O golden
+// Replays tests/golden/io/cases.txt (written by the reference itself,
+// tests/golden/make_io_golden.py): the delimited reader / writer, the model
+// file, the metrics CSV, synth_planted / synth_ratings and the index maps must
+// give the reference's bytes, values, exception classes and messages.
+std::vector<std::string> split(const std::string& s, char sep) {
+  std::vector<std::string> out;
+  std::size_t start = 0;
+  for (std::size_t i = 0; i <= s.size(); ++i)
+    if (i == s.size() || s[i] == sep) {
+      out.push_back(s.substr(start, i - start));
+      start = i + 1;
+    }
+  return out;
+}
+
+std::vector<std::uint32_t> u32_list(const std::string& s) {
+  std::vector<std::uint32_t> v;
+  if (s == "-" || s.empty()) return v;
+  for (const auto& x : split(s, ',')) v.push_back(static_cast<std::uint32_t>(std::stoull(x)));
+  return v;
+}
+
+std::string slurp(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return "<missing " + path + ">";
+  std::string b;
+  char buf[1 << 14];
+  std::size_t n;
+  while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) b.append(buf, n);
+  std::fclose(f);
+  return b;
+}
+
+// code of the exception class (sgdt.h numbering) and its message
+template <class F>
+std::pair<int, std::string> outcome(F&& f) {
+  try {
+    f();
+  } catch (const DataError& e) {  // FormatError is a DataError
+    return {3, e.what()};
+  } catch (const ConfigError& e) {
+    return {2, e.what()};
+  } catch (const NumericError& e) {
+    return {4, e.what()};
+  } catch (const DomainError& e) {
+    return {5, e.what()};
+  } catch (const std::exception& e) {
+    return {1, e.what()};
+  }
+  return {0, ""};
+}
+
+void test_io_golden(const std::string& dir, const char* chunk_bytes) {
+  if (chunk_bytes)
+    setenv("SPTUCKER_LOAD_CHUNK_BYTES", chunk_bytes, 1);
+  else
+    unsetenv("SPTUCKER_LOAD_CHUNK_BYTES");
+  char tmpl[] = "/tmp/sptucker_io_XXXXXX";
+  const std::string out = mkdtemp(tmpl);
+  char cwd[4096];
+  CHECK(getcwd(cwd, sizeof cwd) != nullptr);
+  CHECK(chdir(dir.c_str()) == 0);
+  const std::string cases = slurp("cases.txt");
+  int n_cases = 0;
+  for (const std::string& line : split(cases, '\n')) {
+    if (line.empty()) continue;
+    const std::vector<std::string> f = split(line, '\t');
+    ++n_cases;
+    g_case = "io golden: " + f[0] + " " + f[1];
+    const std::string kind = f[0];
+    if (kind == "load") {
+      LoadOptions o;
+      o.skip_header = f[3] == "1";
+      o.zero_policy = f[4] == "1" ? ZeroPolicy::Replace : ZeroPolicy::Reject;
+      o.zero_replacement = std::stod(f[5]);
+      o.dims_override = u32_list(f[6]);
+      const std::string saved = out + "/" + f[9];
+      const auto [code, msg] = outcome([&] {
+        const CooTensor t = CooTensor::load_delimited(f[1], std::stoul(f[2]), o);
+        CHECK(t.shape().dims() == u32_list(f[8]));
+        t.save_delimited(saved);
+      });
+      CHECK(code == std::stoi(f[7]));
+      CHECK(msg == f[10]);
+      if (code == 0) CHECK(slurp(saved) == slurp(f[9]));
+      if (code != std::stoi(f[7]) || msg != f[10]) std::fprintf(stderr, "  got %d '%s'\n", code, msg.c_str());
+    } else if (kind == "modelgen") {
+      const TuckerModel m = TuckerModel::init_gaussian(Shape(u32_list(f[1])), Ranks{u32_list(f[2]),
+                                                       static_cast<std::uint32_t>(std::stoul(f[3]))},
+                                                       std::stod(f[4]), std::stod(f[5]), std::stoull(f[6]));
+      m.save(out + "/gen.bin");
+      CHECK(slurp(out + "/gen.bin") == slurp(f[7]));
+      const TuckerModel back = TuckerModel::load(f[7]);
+      for (std::size_t n = 0; n < m.order(); ++n) {
+        CHECK(back.factor(n) == m.factor(n));
+        CHECK(back.kruskal(n) == m.kruskal(n));
+      }
+    } else if (kind == "model") {
+      const auto [code, msg] = outcome([&] {
+        const TuckerModel m = TuckerModel::load(f[1]);
+        m.save(out + "/" + f[3]);
+      });
+      CHECK(code == std::stoi(f[2]));
+      CHECK(msg == f[4]);
+      if (code == 0) CHECK(slurp(out + "/" + f[3]) == slurp(f[3]));
+      if (code != std::stoi(f[2]) || msg != f[4]) std::fprintf(stderr, "  got %d '%s'\n", code, msg.c_str());
+    } else if (kind == "mwrite") {
+      std::vector<std::string> comments = split(f[2], '|');
+      std::vector<EpochMetrics> rows;
+      for (const std::string& r : split(f[3], ';')) {
+        std::vector<double> x;
+        for (const std::string& v : split(r, ',')) x.push_back(std::strtod(v.c_str(), nullptr));
+        EpochMetrics m;
+        m.epoch = static_cast<std::size_t>(x[0]);
+        m.core_s = x[1];
+        m.factor_s = x[2];
+        m.total_s = x[3];
+        m.train_rmse = x[4];
+        m.train_mae = x[5];
+        m.test_rmse = x[6];
+        m.test_mae = x[7];
+        m.peak_bytes = static_cast<std::uint64_t>(x[8]);
+        m.comm_bytes = static_cast<std::uint64_t>(x[9]);
+        rows.push_back(m);
+      }
+      write_metrics_csv(out + "/m.csv", rows, comments);
+      CHECK(slurp(out + "/m.csv") == slurp(f[1]));
+    } else if (kind == "mparse") {
+      std::vector<std::string> comments;
+      std::size_t nrows = 0;
+      const auto [code, msg] = outcome([&] { nrows = parse_metrics_csv(f[1], &comments).size(); });
+      CHECK(code == std::stoi(f[2]));
+      CHECK(msg == f[5]);
+      if (code == 0) {
+        CHECK(nrows == std::stoul(f[3]));
+        std::string joined;
+        for (std::size_t i = 0; i < comments.size(); ++i) joined += (i ? "|" : "") + comments[i];
+        CHECK(joined == f[4]);
+      }
+    } else if (kind == "planted") {
+      PlantedSpec p;
+      p.shape = Shape(u32_list(f[1]));
+      p.teacher_ranks = Ranks{u32_list(f[2]), static_cast<std::uint32_t>(std::stoul(f[3]))};
+      p.nnz = std::stoul(f[4]);
+      p.noise_stddev = std::stod(f[5]);
+      p.teacher_mean = std::stod(f[6]);
+      p.teacher_stddev = std::stod(f[7]);
+      p.seed = std::stoull(f[8]);
+      synth_planted(p).save_delimited(out + "/p.tns");
+      CHECK(slurp(out + "/p.tns") == slurp(f[9]));
+    } else if (kind == "ratings") {
+      RatingSpec r;
+      r.base.shape = Shape(u32_list(f[1]));
+      r.base.teacher_ranks = Ranks{u32_list(f[2]), static_cast<std::uint32_t>(std::stoul(f[3]))};
+      r.base.nnz = std::stoul(f[4]);
+      r.base.teacher_mean = std::stod(f[5]);
+      r.base.teacher_stddev = std::stod(f[6]);
+      r.base.seed = std::stoull(f[7]);
+      r.target_mean = std::stod(f[8]);
+      r.target_stddev = std::stod(f[9]);
+      r.noise_stddev = std::stod(f[10]);
+      r.quantize_half_steps = f[11] == "1";
+      r.min_value = std::stod(f[12]);
+      r.max_value = std::stod(f[13]);
+      synth_ratings(r).save_delimited(out + "/r.tns");
+      CHECK(slurp(out + "/r.tns") == slurp(f[14]));
+    } else if (kind == "index") {
+      const Shape shape(u32_list(f[1]));
+      const std::vector<std::uint32_t> c = u32_list(f[2]);
+      const std::size_t mode = std::stoul(f[3]);
+      std::uint64_t col = 0, vec = 0;
+      std::vector<std::uint32_t> inv(c.size());
+      const auto [code, msg] = outcome([&] {
+        col = unfold_col_index(shape, c, mode);
+        vec = vec_index(shape, c, mode);
+        invert_vec_index(shape, vec, mode, inv);
+      });
+      CHECK(code == std::stoi(f[4]));
+      CHECK(msg == f[8]);
+      if (code == 0) {
+        CHECK(col == std::stoull(f[5]));
+        CHECK(vec == std::stoull(f[6]));
+        CHECK(inv == u32_list(f[7]));
+      }
+    } else {
+      CHECK(!"unknown golden case kind");
+    }
+  }
+  CHECK(n_cases > 60);
+  CHECK(chdir(cwd) == 0);
+  std::filesystem::remove_all(out);
+  unsetenv("SPTUCKER_LOAD_CHUNK_BYTES");
+}
+
+// save -> load round trips of the host I/O on generated data (no golden).
+void test_io_round_trips() {
+  char tmpl[] = "/tmp/sptucker_rt_XXXXXX";
+  const std::string out = mkdtemp(tmpl);
+  const Data d = planted({60, 50, 40, 3}, {3, 3, 3, 2}, 2, 5000, 0.1, 0.5, 0.1, 21);
+  const CooTensor t = to_tensor(d);
+  t.save_delimited(out + "/t.tns");
+  setenv("SPTUCKER_LOAD_CHUNK_BYTES", "1000", 1);
+  const CooTensor back = CooTensor::load_delimited(out + "/t.tns", 4);
+  unsetenv("SPTUCKER_LOAD_CHUNK_BYTES");
+  CHECK(back.coords() == t.coords());
+  CHECK(back.values() == t.values());  // %.17g round-trips fp64 exactly
+  for (std::size_t n = 0; n < 4; ++n) {
+    CHECK(back.mode_perm(n) == t.mode_perm(n));
+    CHECK(back.mode_offsets(n) == t.mode_offsets(n));
+  }
+  TuckerModel m = TuckerModel::init_gaussian(t.shape(), Ranks{{3, 3, 3, 2}, 2}, 0.0, 1.0, 4);
+  m.save(out + "/m.bin");
+  const TuckerModel mb = TuckerModel::load(out + "/m.bin");
+  for (std::size_t n = 0; n < 4; ++n) CHECK(mb.factor(n) == m.factor(n) && mb.kruskal(n) == m.kruskal(n));
+  // planted generator == the pinned oracle's, bit for bit
+  PlantedSpec p;
+  p.shape = Shape({60, 50, 40, 3});
+  p.teacher_ranks = Ranks{{3, 3, 3, 2}, 2};
+  p.nnz = 5000;
+  p.noise_stddev = 0.1;
+  p.seed = 21;
+  const CooTensor s = synth_planted(p);
+  CHECK(s.coords() == d.coords);
+  CHECK(s.values() == d.values);
+  std::filesystem::remove_all(out);
+}
+
 void run(const char* name, const std::function<void()>& f) {
   g_case = name;
   const int before = g_fail;
@@ -365,8 +598,20 @@ void run(const char* name, const std::function<void()>& f) {
 }  // namespace
 
 int main(int argc, char** argv) {
+  bool cpu_only = false;
+  std::string golden;
+  for (int i = 1; i < argc; ++i) {
+    const std::string a = argv[i];
+    if (a == "--cpu-only") cpu_only = true;
+    if (a == "--golden" && i + 1 < argc) golden = argv[++i];
+  }
   run("rng engine", test_rng_engine_matches_mt19937_64);
-  if (argc > 1 && std::string(argv[1]) == "--cpu-only") {  // no device in the build container
+  run("io round trips", test_io_round_trips);
+  if (!golden.empty()) {
+    run("io golden (1 thread chunking)", [&] { test_io_golden(golden, nullptr); });
+    run("io golden (512-byte chunks)", [&] { test_io_golden(golden, "512"); });
+  }
+  if (cpu_only) {  // no device in the build container
     run("config errors", test_config_errors);
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;

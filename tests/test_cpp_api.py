@@ -27,7 +27,13 @@ API = [
     "sptucker::comm_cost_report(", "sptucker::CooTensor::CooTensor(", "sptucker::Shape::Shape(",
     "sptucker::TuckerModel::init_gaussian(", "sptucker::TuckerModel::predict(",
     "sptucker::HyperParams::validate(",
+    # host I/O and generators
+    "sptucker::CooTensor::load_delimited(", "sptucker::CooTensor::save_delimited(",
+    "sptucker::TuckerModel::save(", "sptucker::TuckerModel::load(", "sptucker::write_metrics_csv(",
+    "sptucker::parse_metrics_csv(", "sptucker::synth_planted(", "sptucker::synth_ratings(",
+    "sptucker::unfold_col_index(", "sptucker::vec_index(", "sptucker::invert_vec_index(",
 ]
+GOLDEN_IO = os.path.join(ROOT, "tests", "golden", "io")
 
 
 def test_cpp_api_exports(built):
@@ -42,14 +48,14 @@ def test_cpp_api_exports(built):
 
 def test_cpp_suite_cpu_part(built):
     _, exe = built
-    r = subprocess.run([exe, "--cpu-only"], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([exe, "--cpu-only", "--golden", GOLDEN_IO], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.gpu
 def test_cpp_suite_on_gpu(built):
     _, exe = built
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    r = subprocess.run([exe, "--golden", GOLDEN_IO], capture_output=True, text=True, timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert re.search(r"\d+ checks, 0 failures", r.stdout)
