@@ -24,6 +24,7 @@
 // association everywhere -> run-to-run bit identical.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "sgdt_internal.cuh"
@@ -41,6 +42,7 @@ struct FactorArgs {
   const float* val;                      // nnz
   const uint32_t* oidx[kMaxOrder - 1];   // other modes' coordinates (mode-n copy)
   const float* oq[kMaxOrder - 1];        // other modes' Q tables
+  uint32_t orows[kMaxOrder - 1];         // their row counts
   uint64_t nnz;
   const uint32_t* row_ptr;
   const Chunk* chunks;
@@ -273,16 +275,27 @@ constexpr int factor_min_blocks() {
 // are gathered; per-lane partial sums stay in fp32 (a chunk holds at most
 // chunk_size entries, i.e. <= chunk_size/32 terms per lane) and are widened
 // to fp64 at every row boundary.
-template <int RP, int NO>
-__global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
-  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
-  __shared__ __align__(16) float wscr[8 * kWarpScratch];
-  load_bsn<RP>(a, bsn);
-  __syncthreads();
+//
+// SJ >= 0: the other-mode table j == SJ (small, e.g. the 2200-row Q^(3) of
+// BASELINE config 2) was staged into shared memory by the kernel and its
+// gathers are LDS.128: a random-row LDG.128 costs one L1 wavefront per lane,
+// an LDS.128 over 8 banks-groups about 2.6 per 8 lanes, and the L1 data pipe
+// is what bounds this kernel (profiles/r01_ncu_summary.md).
+template <int RP, int SJ>
+__device__ __forceinline__ const float4* q_row(const FactorArgs& a, int j, uint32_t idx, const float4* qs) {
+  if (j == SJ) return qs + static_cast<uint64_t>(idx) * (RP / 4);
+  return reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(idx) * RP);
+}
+template <int RP, int SJ>
+__device__ __forceinline__ float4 q_ld(const float4* p, int j) {
+  if (j == SJ) return *p;
+  return __ldg(p);
+}
+
+template <int RP, int NO, int SJ>
+__device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn, float* wsc, uint32_t wid,
+                                           const float4* qs) {
   const uint32_t lane = threadIdx.x & 31;
-  float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
-  const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid >= a.n_chunks) return;
   const Chunk ch = a.chunks[wid];
   const float* Qn = a.P.Q[a.n];
 
@@ -309,11 +322,10 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
         for (int r = 0; r < RP; ++r) c[r] = 1.f;
 #pragma unroll
         for (int j = 0; j < NO; ++j) {
-          const float4* qk =
-              reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ld_stream(a.oidx[j] + q)) * RP);
+          const float4* qk = q_row<RP, SJ>(a, j, ld_stream(a.oidx[j] + q), qs);
 #pragma unroll
           for (int r = 0; r < RP / 4; ++r) {
-            const float4 t = __ldg(qk + r);
+            const float4 t = q_ld<RP, SJ>(qk + r, j);
             c[4 * r] *= t.x;
             c[4 * r + 1] *= t.y;
             c[4 * r + 2] *= t.z;
@@ -378,9 +390,9 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
       float4 g[NO][RP / 4];
 #pragma unroll
       for (int j = 0; j < NO; ++j) {
-        const float4* qk = reinterpret_cast<const float4*>(a.oq[j] + static_cast<uint64_t>(ik[j]) * RP);
+        const float4* qk = q_row<RP, SJ>(a, j, ik[j], qs);
 #pragma unroll
-        for (int r = 0; r < RP / 4; ++r) g[j][r] = __ldg(qk + r);
+        for (int r = 0; r < RP / 4; ++r) g[j][r] = q_ld<RP, SJ>(qk + r, j);
       }
       const float4* qn = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP);
       float4 h[RP / 4];
@@ -501,6 +513,37 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
 #pragma unroll
     for (int r = 0; r < RP; ++r) dst[r] = static_cast<double>(tot[r]);
   }
+}
+
+template <int RP, int NO>
+__global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
+  __shared__ __align__(16) float wscr[8 * kWarpScratch];
+  load_bsn<RP>(a, bsn);
+  __syncthreads();
+  const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid < a.n_chunks) chunk_body<RP, NO, -1>(a, bsn, wscr + (threadIdx.x >> 5) * kWarpScratch, wid, nullptr);
+}
+
+// Staged variant: persistent CTAs of kStagedWarps warps copy table SJ into
+// shared memory once, then stride over the chunks.
+constexpr int kStagedWarps = 24;
+template <int RP, int NO, int SJ>
+__global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(FactorArgs a) {
+  __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
+  __shared__ __align__(16) float wscr[kStagedWarps * kWarpScratch];
+  extern __shared__ float4 qs[];
+  load_bsn<RP>(a, bsn);
+  {
+    const float4* src = reinterpret_cast<const float4*>(a.oq[SJ]);
+    const uint32_t n4 = a.orows[SJ] * (RP / 4);
+    for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) qs[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
+  for (uint32_t wid = blockIdx.x * kStagedWarps + (threadIdx.x >> 5); wid < a.n_chunks;
+       wid += gridDim.x * kStagedWarps)
+    chunk_body<RP, NO, SJ>(a, bsn, wsc, wid, qs);
 }
 
 // ---------------------------------------------------------------------------
@@ -770,6 +813,58 @@ __global__ void __launch_bounds__(256) factor_finish_kernel(FactorArgs a, uint32
   finalize_row<RP>(a, bsn, rows[t], g);
 }
 
+// Shared-memory staging of one other-mode table (factor_staged_kernel): the
+// smallest table that fits kStageBytes, for RP <= 12 and orders 2-4.
+// SGDT_STAGE=0 turns it off (A/B runs).
+constexpr uint32_t kStageBytes = 104 * 1024;
+template <int RP, int NO>
+int staged_table(const FactorArgs& a) {
+  if (RP > 12 || NO > 3) return -1;
+  static const bool off = [] {
+    const char* e = getenv("SGDT_STAGE");
+    return e && atoi(e) == 0;
+  }();
+  if (off) return -1;
+  int best = -1;
+  for (int j = 0; j < NO; ++j)
+    if (static_cast<uint64_t>(a.orows[j]) * RP * sizeof(float) <= kStageBytes &&
+        (best < 0 || a.orows[j] < a.orows[best]))
+      best = j;
+  return best;
+}
+
+template <int RP, int NO, int SJ>
+cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
+  if constexpr (SJ >= NO || RP > 12 || NO > 3) {
+    return cudaErrorInvalidValue;
+  } else {
+    const size_t smem = static_cast<size_t>(a.orows[SJ]) * RP * sizeof(float);
+    auto kern = factor_staged_kernel<RP, NO, SJ>;
+    // per device (a process may drive several), cheap host calls
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageBytes));
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStagedWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    const int per_sm = occ < 1 ? 1 : occ;
+    const uint32_t need = (a.n_chunks + kStagedWarps - 1) / kStagedWarps;
+    const uint32_t grid = std::min<uint32_t>(need, static_cast<uint32_t>(per_sm) * s.num_sms);
+    kern<<<grid, kStagedWarps * 32, smem, s.stream>>>(a);
+    return cudaGetLastError();
+  }
+}
+
+template <int RP, int NO>
+cudaError_t staged_launch(Session& s, const FactorArgs& a, int sj) {
+  switch (sj) {
+    case 0: return staged_launch_j<RP, NO, 0>(s, a);
+    case 1: return staged_launch_j<RP, NO, 1>(s, a);
+    case 2: return staged_launch_j<RP, NO, 2>(s, a);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int RP, int NO>
 int factor_launch(Session& s, FactorArgs& a) {
   const int block = 256, wpb = block / 32;
@@ -779,9 +874,13 @@ int factor_launch(Session& s, FactorArgs& a) {
       const char* e = getenv("SGDT_GROUP_KERNEL");
       return e && atoi(e) != 0;
     }();
+    const int sj = RP >= 16 || force_group ? -1 : staged_table<RP, NO>(a);
     if (RP >= 16 || force_group)
       factor_group_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
-    else
+    else if (sj >= 0) {
+      const cudaError_t e = staged_launch<RP, NO>(s, a, sj);
+      SGDT_CUDA(e);
+    } else
       factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
     ++s.launches;
@@ -833,6 +932,7 @@ FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h, bool subse
     if (k == n) continue;
     a.oidx[j] = rec.idx + static_cast<uint64_t>(k) * rec.nnz;
     a.oq[j] = s.P.Q[k];
+    a.orows[j] = s.dims[k];
     ++j;
   }
   a.nnz = rec.nnz;
