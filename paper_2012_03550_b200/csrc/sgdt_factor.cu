@@ -49,6 +49,7 @@ struct FactorArgs {
   uint32_t n_chunks;
   const SplitRow* splits;
   uint32_t n_splits;
+  uint32_t n_big_splits;  // splits[0, n_big_splits): one CTA each; the rest one warp each
   double* piece;   // n_pieces x RP
   double* xport;   // 2 x RP: summed pieces of rows cut by this rank's slice
   uint64_t qbase;  // row_ptr value of the copy's first record (shard slice start)
@@ -769,26 +770,54 @@ __global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
   }
 }
 
-// Rows longer than a chunk: sum their pieces in piece order, then finalise.
+// Rows longer than a chunk: sum their pieces, then finalise.  Blocks
+// [0, n_big_splits) take one split row with > kSplitBig pieces each: thread t
+// sums pieces t, t + 256, ... (fp64), each warp reduces with a butterfly and
+// thread 0 adds the eight warp sums in warp order.  (A Zipf head row of
+// BASELINE config 2 has ~6000 pieces; summing it with one warp made this
+// kernel 50-70 us per mode.)  The later blocks give each warp one short split
+// row (lane-strided sum, butterfly).  Fixed association either way, so the
+// result is run-to-run identical.
+constexpr int kSplitThreads = 256;
 template <int RP>
-__global__ void __launch_bounds__(256) factor_split_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(kSplitThreads) factor_split_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
+  __shared__ double part[kSplitThreads / 32][RP];
   load_bsn<RP>(a, bsn);
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid >= a.n_splits) return;
-  const SplitRow sr = a.splits[wid];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool big = blockIdx.x < a.n_big_splits;
+  const uint32_t idx = big ? blockIdx.x : a.n_big_splits + (blockIdx.x - a.n_big_splits) * (kSplitThreads / 32) + warp;
+  const bool have = idx < a.n_splits;
+  SplitRow sr{};
+  if (have) sr = a.splits[idx];
   double g[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) g[r] = 0.0;
-  for (uint32_t p = lane; p < sr.count; p += 32) {
-    const double* src = a.piece + static_cast<uint64_t>(sr.first + p) * RP;
+  const uint32_t t0 = big ? threadIdx.x : lane, step = big ? kSplitThreads : 32;
+  if (have)
+    for (uint32_t p = t0; p < sr.count; p += step) {
+      const double* src = a.piece + static_cast<uint64_t>(sr.first + p) * RP;
 #pragma unroll
-    for (int r = 0; r < RP; ++r) g[r] += src[r];
-  }
+      for (int r = 0; r < RP; ++r) g[r] += src[r];
+    }
   warp_allreduce<RP>(g);
-  if (lane != 0) return;
+  if (big) {
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) part[warp][r] = g[r];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      double t = part[0][r];
+      for (int w = 1; w < kSplitThreads / 32; ++w) t += part[w][r];
+      g[r] = t;
+    }
+  } else {
+    __syncthreads();  // bsn
+    if (!have || lane != 0) return;
+  }
   if (sr.pad) {  // cut by the slice edge: export for the rank-ordered merge
     double* dst = a.xport + static_cast<uint64_t>(sr.pad - 1) * RP;
 #pragma unroll
@@ -886,8 +915,9 @@ int factor_launch(Session& s, FactorArgs& a) {
     ++s.launches;
   }
   if (a.n_splits) {
-    const unsigned grid = (a.n_splits + wpb - 1) / wpb;
-    factor_split_kernel<RP><<<grid, block, 0, s.stream>>>(a);
+    const uint32_t wpb_s = kSplitThreads / 32;
+    const unsigned grid = a.n_big_splits + (a.n_splits - a.n_big_splits + wpb_s - 1) / wpb_s;
+    factor_split_kernel<RP><<<grid, kSplitThreads, 0, s.stream>>>(a);
     SGDT_CUDA(cudaGetLastError());
     ++s.launches;
   }
@@ -941,6 +971,7 @@ FactorArgs factor_args(Session& s, int n, const sgdt_factor_hyper& h, bool subse
   a.n_chunks = subset ? rs.n_chunks : mp.n_chunks;
   a.splits = subset ? rs.splits : mp.splits;
   a.n_splits = subset ? rs.n_splits : mp.n_splits;
+  a.n_big_splits = subset ? rs.n_big_splits : mp.n_big_splits;
   a.piece = s.piece_partials;
   a.xport = s.export_buf;
   a.qbase = subset ? 0 : mp.shard.qb;

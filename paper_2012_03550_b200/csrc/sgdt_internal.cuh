@@ -28,6 +28,9 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 // piece < 0: the chunk holds whole rows; otherwise it is piece `piece` of a
 // row longer than the chunk size (finalised by the split-row kernel).
 // pad = 1: whole rows that are all short -- one row per lane.
+// Split rows with more pieces than this are reduced by a whole CTA.
+constexpr uint32_t kSplitBig = 64;
+
 struct Chunk {
   uint32_t begin;
   uint32_t end;
@@ -83,6 +86,7 @@ struct RowSubset {
   uint32_t n_chunks = 0;
   struct SplitRow* splits = nullptr;
   uint32_t n_splits = 0;
+  uint32_t n_big_splits = 0;  // splits[0, n_big_splits) have > kSplitBig pieces
   uint32_t n_pieces = 0;
 };
 
@@ -93,6 +97,7 @@ struct ModePlan {
   uint32_t n_chunks = 0;
   SplitRow* splits = nullptr;
   uint32_t n_splits = 0;
+  uint32_t n_big_splits = 0;  // splits[0, n_big_splits) have > kSplitBig pieces
   uint32_t n_pieces = 0;
   uint64_t rows_nonempty = 0;
   uint64_t rows_empty = 0;

@@ -156,7 +156,9 @@ constexpr uint64_t kShortRow = 64;
 // (the rank-ordered boundary merge of factor_optimizer.cpp:247-270).  Chunk
 // bounds are relative to qb.
 void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, uint32_t chunk_size,
-                  std::vector<Chunk>& chunks, std::vector<SplitRow>& splits, uint32_t& n_pieces, ShardPlan& sp) {
+                  std::vector<Chunk>& chunks, std::vector<SplitRow>& splits, uint32_t& n_pieces, ShardPlan& sp,
+                  uint32_t& n_big) {
+  n_big = 0;
   chunks.clear();
   splits.clear();
   n_pieces = 0;
@@ -207,6 +209,9 @@ void build_chunks(const std::vector<uint64_t>& off, uint64_t qb, uint64_t qe, ui
     if (cnt >= kShortRow) cur.pad = 0;  // pad = 1: every row of the chunk is short
   }
   close();
+  // split rows with many pieces first (one CTA each in factor_split_kernel)
+  std::stable_partition(splits.begin(), splits.end(), [](const SplitRow& r) { return r.count > kSplitBig; });
+  for (const SplitRow& r : splits) n_big += r.count > kSplitBig;
 }
 
 // Intra-row order of the mode-n copy.  The reference visits a row's entries in
@@ -630,7 +635,7 @@ int ensure_subset(Session& s, int n, double fraction) {
   std::vector<Chunk> chunks;
   std::vector<SplitRow> splits;
   ShardPlan sp;
-  build_chunks(sub, 0, T, s.chunk_size, chunks, splits, rs.n_pieces, sp);
+  build_chunks(sub, 0, T, s.chunk_size, chunks, splits, rs.n_pieces, sp, rs.n_big_splits);
   rs.n_chunks = static_cast<uint32_t>(chunks.size());
   rs.n_splits = static_cast<uint32_t>(splits.size());
   TRY(dalloc(&rs.chunks, chunks.size()));
@@ -833,7 +838,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
                                 s->stream));
       std::vector<Chunk> chunks;
       std::vector<SplitRow> splits;
-      build_chunks(off, qb, qe, s->chunk_size, chunks, splits, mp.n_pieces, mp.shard);
+      build_chunks(off, qb, qe, s->chunk_size, chunks, splits, mp.n_pieces, mp.shard, mp.n_big_splits);
       mp.rows_nonempty = 0;
       for (size_t i = 0; i + 1 < off.size(); ++i) mp.rows_nonempty += off[i + 1] > off[i];
       mp.rows_empty = s->dims[n] - mp.rows_nonempty;
