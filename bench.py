@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="override the per-config CPU sample size")
+    p.add_argument("--row-fraction", type=float, default=1.0,
+                   help="FactorHyper::row_fraction of our arm (diagnostics; the headline uses 1.0)")
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (sharded factor phase) driver even on one rank")
     return p.parse_args()
@@ -374,7 +376,7 @@ def run_ours(args, rank, world, local_rank):
     s.set_model(A, B)
     s.seed(HYPER["seed"] + 1)
     ch = sgdt.CoreHyper(HYPER["lr_b"], HYPER["reg_b"], m, 0, 0)
-    fh = sgdt.FactorHyper(HYPER["lr_a"], HYPER["reg_a"], 1.0)
+    fh = sgdt.FactorHyper(HYPER["lr_a"], HYPER["reg_a"], args.row_fraction)
     for _ in range(args.warmup):
         s.run_epochs(ch, fh, 1)
 
@@ -399,7 +401,9 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     timing = s.last_timing()
-    units = units_per_epoch(order, m, nnz)
+    # N (M + f nnz); f < 1 keeps max(1, llround(f |bucket|)) per row,
+    # f nnz is its nominal size
+    units = units_per_epoch(order, m, nnz) if args.row_fraction == 1.0 else int(order * (m + args.row_fraction * nnz))
     value = units * args.steps * world / (elapsed_ms * 1e-3)
     ms_per_step = elapsed_ms / args.steps
 
@@ -477,7 +481,7 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
             "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz_total": spec.nnz,
-                       "nnz_train": nnz, "J": J, "R": R, "batch_m": m, "units_per_step": units,
+                       "nnz_train": nnz, "J": J, "R": R, "batch_m": m, "row_fraction": args.row_fraction, "units_per_step": units,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "COO record copies (4 x 16 B x nnz) exceed the 126 MB L2; Q tables are L2-resident by design",
                        "test_rmse_after": rmse, "data_gen_s": data["gen_s"], "setup_s": setup_s},

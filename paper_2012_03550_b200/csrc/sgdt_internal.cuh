@@ -28,6 +28,15 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 // piece < 0: the chunk holds whole rows; otherwise it is piece `piece` of a
 // row longer than the chunk size (finalised by the split-row kernel).
 // pad = 1: whole rows that are all short -- one row per lane.
+// Jump-ahead of the mt19937_64 engine for long draw runs (sgdt_sampler.cu):
+// J = T^L (column-major, 19968 x 312 words) and the segment starts.
+struct MtJump {
+  uint64_t* J = nullptr;
+  uint64_t* st = nullptr;
+  uint64_t st_cap = 0;
+  uint64_t* part = nullptr;
+};
+
 // Split rows with more pieces than this are reduced by a whole CTA.
 constexpr uint32_t kSplitBig = 64;
 
@@ -152,6 +161,11 @@ struct Session {
 
   // sampler state
   uint64_t* mt = nullptr;       // 312 words + position word
+  uint64_t* mt_out = nullptr;   // raw engine outputs of the last draw run (mt_gen_kernel)
+  uint64_t mt_out_cap = 0;
+  uint64_t* mt_tent = nullptr;  // 313: the engine state after the run if nothing was rejected
+  int* mt_flag = nullptr;       // set by draw_map_kernel when an output was rejected
+  MtJump jump;                  // jump-ahead of long draw runs (sgdt_sampler.cu)
   uint32_t* pool = nullptr;     // nnz, persistent
   bool pool_valid = false;
   unsigned long long* head = nullptr;  // nnz stamped list heads

@@ -471,6 +471,12 @@ void free_session(sgdt_session* s) {
   F(s->merge_g);
   F(s->d_peers);
   F(s->mt);
+  F(s->mt_out);
+  F(s->mt_tent);
+  F(s->mt_flag);
+  F(s->jump.J);
+  F(s->jump.st);
+  F(s->jump.part);
   F(s->pool);
   F(s->head);
   F(s->draw_j);
@@ -1538,9 +1544,11 @@ int sgdt_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, int device
     return SGDT_OK;
   }();
   for (void* p : {(void*)t.mt, (void*)t.pool, (void*)t.head, (void*)t.draw_j, (void*)t.link, (void*)t.kprev,
-                  (void*)t.lprev, (void*)t.dval, (void*)batch, (void*)keys_out, tmp})
+                  (void*)t.lprev, (void*)t.dval, (void*)batch, (void*)keys_out, tmp, (void*)t.mt_out,
+                  (void*)t.mt_tent, (void*)t.mt_flag, (void*)t.jump.J, (void*)t.jump.st, (void*)t.jump.part})
     if (p) cudaFree(p);
-  t.mt = nullptr;
+  t.mt = t.mt_out = t.mt_tent = nullptr;
+  t.mt_flag = nullptr;
   t.pool = t.draw_j = t.link = t.kprev = t.lprev = t.dval = nullptr;
   t.head = nullptr;
   if (t.stream) cudaStreamDestroy(t.stream);

@@ -123,6 +123,45 @@ def test_next_below_rejection_path_bit_exact():
     assert pos2 == rpos and np.array_equal(st2, rst)
 
 
+@pytest.mark.parametrize("lead", [0, 1, 311, 312, 1000])
+def test_next_below_long_runs_bit_exact(lead):
+    # the parallel path (engine run + grid-wide map, no rejection): many
+    # blocks, starting mid-block, state installed from the recorded end state
+    rs = np.random.default_rng(lead)
+    st, pos = sg().mt19937_64_state(5)
+    r = O.Rng(5)
+    if lead:
+        b0 = rs.integers(1, 2**20, lead, dtype=np.uint64)
+        got0, st, pos = sg().rng_next_below(st, pos, b0)
+        assert np.array_equal(got0, np.array([r.next_below(int(b)) for b in b0], np.uint64))
+    bounds = rs.integers(1, 2**33, 40_000, dtype=np.uint64)
+    got, st2, pos2 = sg().rng_next_below(st, pos, bounds)
+    ref = np.array([r.next_below(int(b)) for b in bounds], np.uint64)
+    assert np.array_equal(got, ref)
+    rst, rpos = r.state()
+    assert pos2 == rpos and np.array_equal(st2, rst)
+    got3, st3, pos3 = sg().rng_next_below(st2, pos2, np.zeros(0, np.uint64))
+    assert len(got3) == 0 and pos3 == pos2 and np.array_equal(st3, st2)
+
+
+@pytest.mark.parametrize("lead,n", [(0, 2_600_000), (7, 3 * 2048 * 312 - 7 + 312), (311, 1_000_003)])
+def test_engine_jump_ahead_segments_bit_exact(monkeypatch, lead, n):
+    # long runs are cut into segments of 2048 blocks started from J^k T B0
+    # (J = T^2048 built bit-sliced on the device); forced on here
+    monkeypatch.setenv("SGDT_JUMP_MIN_BLOCKS", "2")
+    raw = O.mt_outputs(77, lead + n)
+    st, pos = sg().mt19937_64_state(77)
+    if lead:
+        _, st, pos = sg().rng_next_below(st, pos, np.full(lead, 2**63, np.uint64))
+    got, st2, pos2 = sg().rng_next_below(st, pos, np.full(n, 2**40, np.uint64))  # power of 2: no rejection
+    assert np.array_equal(got, raw[lead:] & np.uint64(2**40 - 1))
+    r = O.Rng(77)
+    for _ in range(lead + n):
+        r.next_u64()
+    rst, rpos = r.state()
+    assert pos2 == rpos and np.array_equal(st2, rst)
+
+
 # ---------------------------------------------------------------- eval
 def test_rmse_mae_matches_oracle():
     dims = (30, 25, 20)
