@@ -1082,7 +1082,8 @@ struct CopyOut {
 };
 
 int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
-                    const CopyOut* out);
+                    const CopyOut* out, bool first_sampled = false);
+bool sample_runs_ahead(const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh);
 }  // namespace
 }  // namespace sgdt
 
@@ -1115,6 +1116,18 @@ int sgdt_run_epochs_host(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_
     TRY(dalloc(&s->xfer, total));
     s->xfer_cap = total;
   }
+  // Psi of the first epoch depends only on the RNG: draw it on the side
+  // stream while the model is copied in
+  TRY(settle_ahead(*s, false, "run_epochs_host"));
+  const bool early = epochs > 0 && sample_runs_ahead(ch, fh);
+  if (early) {
+    TRY(ensure_batch_capacity(*s, m));
+    TRY(ensure_core_capacity(*s, m));
+    SGDT_CUDA(cudaEventRecord(s->ev_start, s->stream));
+    SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_start, 0));
+    TRY(enqueue_sample(*s, *ch, m, s->batch, s->side));
+    SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+  }
   // load: the copies back to back, then the casts
   for (int k = 0; k < s->order; ++k) {
     const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k], nb = static_cast<uint64_t>(s->J[k]) * s->R;
@@ -1135,15 +1148,22 @@ int sgdt_run_epochs_host(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_
     SGDT_CUDA(cudaStreamSynchronize(s->stream));
     return sgdt_get_model(s, A_out, B_out);
   }
-  return run_epochs_impl(s, ch, fh, epochs, &co);
+  return run_epochs_impl(s, ch, fh, epochs, &co, early);
 }
 
 }  // extern "C"
 
 namespace sgdt {
 namespace {
+// Psi does not depend on the model, so epoch e+1's sampler can run on the
+// side stream during epoch e (with row_fraction < 1 the factor phase also
+// draws, so no run-ahead).
+bool sample_runs_ahead(const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh) {
+  return ch->lr > 0.0 && ch->batch_m != 0 && !(fh->lr > 0.0 && fh->row_fraction < 1.0);
+}
+
 int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_factor_hyper* fh, uint64_t epochs,
-                    const CopyOut* out) {
+                    const CopyOut* out, bool first_sampled) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   uint64_t m = 0;
   TRY(check_core_hyper(*s, ch, &m));
@@ -1156,17 +1176,19 @@ int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
   // stream is consumed in exactly the reference order: the factor phase draws
   // nothing (row_fraction == 1).
   // (with row_fraction < 1 the factor phase also draws, so no run-ahead)
-  const bool ahead = ch->lr > 0.0 && ch->batch_m != 0 && !(fh->lr > 0.0 && fh->row_fraction < 1.0);
+  const bool ahead = sample_runs_ahead(ch, fh);
   uint32_t* buf[2] = {nullptr, nullptr};
   if (ahead) {
     TRY(ensure_batch_capacity(*s, m));
     TRY(ensure_core_capacity(*s, m));
     buf[0] = s->batch;
     buf[1] = s->batch + static_cast<uint64_t>(s->order) * m;
-    SGDT_CUDA(cudaEventRecord(s->ev_start, s->stream));
-    SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_start, 0));
-    TRY(enqueue_sample(*s, *ch, m, buf[0], s->side));
-    SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+    if (!first_sampled) {  // (run_epochs_host drew it before its copies)
+      SGDT_CUDA(cudaEventRecord(s->ev_start, s->stream));
+      SGDT_CUDA(cudaStreamWaitEvent(s->side, s->ev_start, 0));
+      TRY(enqueue_sample(*s, *ch, m, buf[0], s->side));
+      SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
+    }
   }
   for (uint64_t e = 0; e < epochs; ++e) {
     const bool last = e + 1 == epochs;
