@@ -140,17 +140,8 @@ def make_data(cfg: int, scale: float, device):
     if scale != 1.0:
         spec = synth.scaled(spec, scale ** (1.0 / len(spec.dims)), int(spec.nnz * scale))
     t0 = time.time()
-    (trc, trv), (tec, tev), perms = synth.generate(spec, device)
-    torch.cuda.synchronize()
-    data = dict(
-        spec=spec,
-        train=(trc.cpu().numpy().astype(np.uint32), trv.cpu().numpy()),
-        test=(tec.cpu().numpy().astype(np.uint32), tev.cpu().numpy()),
-        gen_s=time.time() - t0,
-    )
-    del trc, trv, tec, tev, perms
-    torch.cuda.empty_cache()
-    return data
+    train, test, _ = synth.generate(spec, device)
+    return dict(spec=spec, train=train, test=test, gen_s=time.time() - t0)
 
 
 def units_per_epoch(order, m, nnz):

@@ -276,6 +276,28 @@ int sgdt_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, int device
 int sgdt_rng_next_below(const uint64_t* mt312, uint32_t pos, const uint64_t* bounds,
                         uint64_t n, uint64_t* out, uint64_t* mt312_out, uint32_t* pos_out);
 
+/* The BASELINE config 2-5 generator (extending
+ * synth.cpp:16-103): nnz distinct positions drawn per mode from a
+ * bounded-support Zipf(zipf[n]) (0 = uniform) with a Philox4x32-10 stream,
+ * first draw wins, ascending linear position (mode 1 fastest, as
+ * synth.cpp:40); values from a planted Kruskal teacher with J = teacher_j,
+ * R = teacher_r, entries N(0, sigma^2), sigma = (J R^(1/N))^(-1/4): ratings
+ * (round(3 + standardised xhat), clipped to [1, 5]) or xhat + noise N(0, 1).
+ * coords (nnz*N, 1-based, entry-major) and values (nnz) are host buffers.
+ * ConfigError when the device runs out of memory. */
+typedef struct {
+  int order;
+  const uint32_t* dims;
+  const double* zipf;
+  uint64_t nnz;
+  uint32_t teacher_j;
+  uint32_t teacher_r;
+  int ratings;
+  double noise;
+  uint64_t seed;
+} sgdt_synth_spec;
+int sgdt_synth(const sgdt_synth_spec* spec, int device, uint32_t* coords, double* values);
+
 /* partition_even (scheduler.cpp:34-46): slice w of count over workers. */
 void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uint64_t* ends);
 

@@ -128,6 +128,7 @@ def load(build_if_missing: bool = True):
     L.sgdt_rng_next_below.argtypes = [u64p, C.c_uint32, u64p, C.c_uint64, u64p, u64p, u32p]
     L.sgdt_partition_even.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p]
     L.sgdt_split_ids.argtypes = [C.c_uint64, C.c_double, C.c_uint64, C.c_int, u32p, u32p]
+    L.sgdt_synth.argtypes = [C.POINTER(SynthSpec), C.c_int, u32p, C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -169,6 +170,27 @@ def split_ids(nnz: int, test_fraction: float, seed: int, device: int = -1):
     tr = np.empty(max(nnz - ntest, 1), np.uint32)
     _ck(_lib.sgdt_split_ids(nnz, test_fraction, seed, device, _p(te, C.c_uint32), _p(tr, C.c_uint32)))
     return te[:ntest], tr[: nnz - ntest]
+
+
+class SynthSpec(C.Structure):
+    _fields_ = [("order", C.c_int), ("dims", C.POINTER(C.c_uint32)), ("zipf", C.POINTER(C.c_double)),
+                ("nnz", C.c_uint64), ("teacher_j", C.c_uint32), ("teacher_r", C.c_uint32),
+                ("ratings", C.c_int), ("noise", C.c_double), ("seed", C.c_uint64)]
+
+
+def synth(dims, zipf, nnz: int, teacher_j: int, teacher_r: int, ratings: bool, noise: float, seed: int,
+          device: int = -1):
+    """sgdt_synth: the config 2-5 tensor generated on the device; returns host
+    (coords uint32 [nnz, N] 1-based, values f64 [nnz]) in linear-position order."""
+    load()
+    d = np.ascontiguousarray(dims, np.uint32)
+    z = np.ascontiguousarray(zipf, np.float64)
+    spec = SynthSpec(len(d), _p(d, C.c_uint32), _p(z, C.c_double), nnz, teacher_j, teacher_r,
+                     1 if ratings else 0, noise, seed)
+    coords = np.empty((nnz, len(d)), np.uint32)
+    values = np.empty(nnz, np.float64)
+    _ck(_lib.sgdt_synth(C.byref(spec), device, _p(coords, C.c_uint32), _p(values, C.c_double)))
+    return coords, values
 
 
 def rng_next_below(state: np.ndarray, pos: int, bounds: np.ndarray):

@@ -17,15 +17,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def c2():
-    import torch
     from paper_2012_03550_b200 import synth
-    (trc, trv), (tec, tev), perms = synth.generate(synth.CONFIGS[2], "cuda", with_perms=True)
-    out = dict(dims=synth.CONFIGS[2].dims, train=(trc.cpu().numpy().astype(np.uint32), trv.cpu().numpy()),
-               test=(tec.cpu().numpy().astype(np.uint32), tev.cpu().numpy()),
-               perms=[p.cpu().numpy().astype(np.uint32) for p in perms])
-    del trc, trv, tec, tev, perms
-    torch.cuda.empty_cache()
-    return out
+    train, test, perms = synth.generate(synth.CONFIGS[2], "cuda", with_perms=True)
+    return dict(dims=synth.CONFIGS[2].dims, train=train, test=test, perms=perms)
 
 
 def session(c2):
