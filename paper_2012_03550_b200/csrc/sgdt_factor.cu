@@ -292,8 +292,20 @@ __device__ __forceinline__ float4 q_ld(const float4* p, int j) {
   if (j == SJ) return *p;
   return __ldg(p);
 }
+// T2: R <= RP - 2, so the last float4 of a row holds two zero pads: load it
+// as a float2 (a random-row LDG.64 costs about half the L1 data-pipe
+// wavefronts of an LDG.128; the product is unchanged, the pads are zero).
+template <int RP, int SJ, bool T2>
+__device__ __forceinline__ float4 q_ld_r(const float4* p, int j, int r) {
+  if (T2 && r == RP / 4 - 1) {
+    const float2* p2 = reinterpret_cast<const float2*>(p);
+    const float2 v = j == SJ ? *p2 : __ldg(p2);
+    return make_float4(v.x, v.y, 0.f, 0.f);
+  }
+  return q_ld<RP, SJ>(p, j);
+}
 
-template <int RP, int NO, int SJ>
+template <int RP, int NO, int SJ, bool T2>
 __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn, float* wsc, uint32_t wid,
                                            const float4* qs) {
   const uint32_t lane = threadIdx.x & 31;
@@ -326,7 +338,7 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
           const float4* qk = q_row<RP, SJ>(a, j, ld_stream(a.oidx[j] + q), qs);
 #pragma unroll
           for (int r = 0; r < RP / 4; ++r) {
-            const float4 t = q_ld<RP, SJ>(qk + r, j);
+            const float4 t = q_ld_r<RP, SJ, T2>(qk + r, j, r);
             c[4 * r] *= t.x;
             c[4 * r + 1] *= t.y;
             c[4 * r + 2] *= t.z;
@@ -393,7 +405,7 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
       for (int j = 0; j < NO; ++j) {
         const float4* qk = q_row<RP, SJ>(a, j, ik[j], qs);
 #pragma unroll
-        for (int r = 0; r < RP / 4; ++r) g[j][r] = q_ld<RP, SJ>(qk + r, j);
+        for (int r = 0; r < RP / 4; ++r) g[j][r] = q_ld_r<RP, SJ, T2>(qk + r, j, r);
       }
       const float4* qn = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP);
       float4 h[RP / 4];
@@ -516,20 +528,20 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
   }
 }
 
-template <int RP, int NO>
+template <int RP, int NO, bool T2>
 __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   __shared__ __align__(16) float wscr[8 * kWarpScratch];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid < a.n_chunks) chunk_body<RP, NO, -1>(a, bsn, wscr + (threadIdx.x >> 5) * kWarpScratch, wid, nullptr);
+  if (wid < a.n_chunks) chunk_body<RP, NO, -1, T2>(a, bsn, wscr + (threadIdx.x >> 5) * kWarpScratch, wid, nullptr);
 }
 
 // Staged variant: persistent CTAs of kStagedWarps warps copy table SJ into
 // shared memory once, then stride over the chunks.
 constexpr int kStagedWarps = 24;
-template <int RP, int NO, int SJ>
+template <int RP, int NO, int SJ, bool T2>
 __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   __shared__ __align__(16) float wscr[kStagedWarps * kWarpScratch];
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(Fac
   float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
   for (uint32_t wid = blockIdx.x * kStagedWarps + (threadIdx.x >> 5); wid < a.n_chunks;
        wid += gridDim.x * kStagedWarps)
-    chunk_body<RP, NO, SJ>(a, bsn, wsc, wid, qs);
+    chunk_body<RP, NO, SJ, T2>(a, bsn, wsc, wid, qs);
 }
 
 // ---------------------------------------------------------------------------
@@ -862,13 +874,13 @@ int staged_table(const FactorArgs& a) {
   return best;
 }
 
-template <int RP, int NO, int SJ>
+template <int RP, int NO, int SJ, bool T2>
 cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
   if constexpr (SJ >= NO || RP > 12 || NO > 3) {
     return cudaErrorInvalidValue;
   } else {
     const size_t smem = static_cast<size_t>(a.orows[SJ]) * RP * sizeof(float);
-    auto kern = factor_staged_kernel<RP, NO, SJ>;
+    auto kern = factor_staged_kernel<RP, NO, SJ, T2>;
     // per device (a process may drive several), cheap host calls
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageBytes));
@@ -884,12 +896,12 @@ cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
   }
 }
 
-template <int RP, int NO>
+template <int RP, int NO, bool T2>
 cudaError_t staged_launch(Session& s, const FactorArgs& a, int sj) {
   switch (sj) {
-    case 0: return staged_launch_j<RP, NO, 0>(s, a);
-    case 1: return staged_launch_j<RP, NO, 1>(s, a);
-    case 2: return staged_launch_j<RP, NO, 2>(s, a);
+    case 0: return staged_launch_j<RP, NO, 0, T2>(s, a);
+    case 1: return staged_launch_j<RP, NO, 1, T2>(s, a);
+    case 2: return staged_launch_j<RP, NO, 2, T2>(s, a);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -906,11 +918,22 @@ int factor_launch(Session& s, FactorArgs& a) {
     const int sj = RP >= 16 || force_group ? -1 : staged_table<RP, NO>(a);
     if (RP >= 16 || force_group)
       factor_group_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
-    else if (sj >= 0) {
-      const cudaError_t e = staged_launch<RP, NO>(s, a, sj);
-      SGDT_CUDA(e);
-    } else
-      factor_chunk_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
+    else {
+      // T2 (half-width tail loads) is instantiated for RP = 12 only (R = 9, 10)
+      static const bool t2_off = [] {  // SGDT_T2=0: full-width tails (A/B runs)
+        const char* e = getenv("SGDT_T2");
+        return e && atoi(e) == 0;
+      }();
+      const bool t2 = RP == 12 && a.P.R + 2 <= RP && !t2_off;
+      if (sj >= 0) {
+        const cudaError_t e = t2 ? staged_launch<RP, NO, RP == 12>(s, a, sj) : staged_launch<RP, NO, false>(s, a, sj);
+        SGDT_CUDA(e);
+      } else if (t2) {
+        factor_chunk_kernel<RP, NO, RP == 12><<<grid, block, 0, s.stream>>>(a);
+      } else {
+        factor_chunk_kernel<RP, NO, false><<<grid, block, 0, s.stream>>>(a);
+      }
+    }
     SGDT_CUDA(cudaGetLastError());
     ++s.launches;
   }
