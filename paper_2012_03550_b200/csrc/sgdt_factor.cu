@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(Fac
   __shared__ __align__(16) float wscr[kStagedWarps * kWarpScratch];
   extern __shared__ float4 qs[];
   load_bsn<RP>(a, bsn);
-  {
+  if constexpr (SJ >= 0) {
     const float4* src = reinterpret_cast<const float4*>(a.oq[SJ]);
     const uint32_t n4 = a.orows[SJ] * (RP / 4);
     for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) qs[i] = __ldg(src + i);
@@ -879,7 +879,7 @@ cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
   if constexpr (SJ >= NO || RP > 12 || NO > 3) {
     return cudaErrorInvalidValue;
   } else {
-    const size_t smem = static_cast<size_t>(a.orows[SJ]) * RP * sizeof(float);
+    const size_t smem = SJ >= 0 ? static_cast<size_t>(a.orows[SJ < 0 ? 0 : SJ]) * RP * sizeof(float) : 0;
     auto kern = factor_staged_kernel<RP, NO, SJ, T2>;
     // per device (a process may drive several), cheap host calls
     cudaError_t e =
@@ -899,6 +899,7 @@ cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
 template <int RP, int NO, bool T2>
 cudaError_t staged_launch(Session& s, const FactorArgs& a, int sj) {
   switch (sj) {
+    case -1: return staged_launch_j<RP, NO, -1, T2>(s, a);  // persistent, no staged table
     case 0: return staged_launch_j<RP, NO, 0, T2>(s, a);
     case 1: return staged_launch_j<RP, NO, 1, T2>(s, a);
     case 2: return staged_launch_j<RP, NO, 2, T2>(s, a);
@@ -925,7 +926,11 @@ int factor_launch(Session& s, FactorArgs& a) {
         return e && atoi(e) == 0;
       }();
       const bool t2 = RP == 12 && a.P.R + 2 <= RP && !t2_off;
-      if (sj >= 0) {
+      static const bool persist = [] {  // SGDT_PERSIST=1: persistent launch without a staged table
+        const char* e = getenv("SGDT_PERSIST");
+        return e && atoi(e) != 0;
+      }();
+      if (sj >= 0 || (persist && RP <= 12 && NO <= 3)) {
         const cudaError_t e = t2 ? staged_launch<RP, NO, RP == 12>(s, a, sj) : staged_launch<RP, NO, false>(s, a, sj);
         SGDT_CUDA(e);
       } else if (t2) {
