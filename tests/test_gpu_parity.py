@@ -267,6 +267,26 @@ def test_small_chunks_force_row_splitting(monkeypatch):
         assert rel_err(A[n], RA[n]) <= TOL
 
 
+@pytest.mark.parametrize("dims,J,R,nnz,chunk", [
+    ((2, 100, 100), (4, 4, 4), 4, 9000, "40"),       # ~4500-entry rows: > 64 pieces, one CTA per split row
+    ((3, 90, 80), (10, 10, 10), 10, 12000, "32"),    # R = 10: half-width Q-row tails, staged table, CTA splits
+    ((2, 70, 60, 5), (5, 5, 5, 5), 5, 8000, "48"),   # order 4
+])
+def test_many_piece_rows_match_oracle(monkeypatch, dims, J, R, nnz, chunk):
+    monkeypatch.setenv("SGDT_CHUNK_SIZE", chunk)
+    tr, _ = make_case(dims, J, R, nnz, 37)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 41)
+    s.set_model(*m.params())
+    s.factor_epoch(0.01, 0.01)
+    O.update_factor_epoch(m, t, 0.01, 0.01, O.Rng(1))
+    A, _ = s.get_model()
+    RA, _ = m.params()
+    for n in range(len(dims)):
+        assert rel_err(A[n], RA[n]) <= TOL
+
+
 def test_free_run_config1_matches_reference_rmse():
     """BASELINE config 1 end to end (10 epochs); the reference's own final
     test RMSE is committed in tests/golden/config1.json."""
