@@ -287,6 +287,25 @@ def test_many_piece_rows_match_oracle(monkeypatch, dims, J, R, nnz, chunk):
         assert rel_err(A[n], RA[n]) <= TOL
 
 
+@pytest.mark.parametrize("dims,J,R,nnz", [
+    ((3000, 60, 50), (32, 32, 32), 32, 20000),        # mode 0: ~7-entry rows, one row per 8-lane group
+    ((2500, 40, 30, 6), (16,) * 4, 16, 15000),        # order 4, R = 16: E = 8 groups
+    ((4000, 50, 40), (24, 20, 20), 20, 16000),        # R = 20: 5-lane groups (non power of two)
+])
+def test_wide_short_rows_match_oracle(dims, J, R, nnz):
+    tr, _ = make_case(dims, J, R, nnz, 43, ts=0.05)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 47, sd=0.05, mean=0.3)
+    s.set_model(*m.params())
+    s.factor_epoch(0.01, 0.01)
+    O.update_factor_epoch(m, t, 0.01, 0.01, O.Rng(1))
+    A, _ = s.get_model()
+    RA, _ = m.params()
+    for n in range(len(dims)):
+        assert rel_err(A[n], RA[n]) <= TOL
+
+
 def test_free_run_config1_matches_reference_rmse():
     """BASELINE config 1 end to end (10 epochs); the reference's own final
     test RMSE is committed in tests/golden/config1.json."""
