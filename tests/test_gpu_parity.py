@@ -293,10 +293,11 @@ def test_many_piece_rows_match_oracle(monkeypatch, dims, J, R, nnz, chunk):
     ((4000, 50, 40), (24, 20, 20), 20, 16000),        # R = 20: 5-lane groups (non power of two)
 ])
 def test_wide_short_rows_match_oracle(dims, J, R, nnz):
-    tr, _ = make_case(dims, J, R, nnz, 43, ts=0.05)
+    sig = unit_sigma(dims, J, R)  # unit-variance teacher and start: a stable step
+    tr, _ = make_case(dims, J, R, nnz, 43, tm=0.0, ts=sig)
     t = O.Tensor(dims, *tr)
     s = session_for(dims, tr, J, R)
-    m = oracle_model(dims, J, R, 47, sd=0.05, mean=0.3)
+    m = oracle_model(dims, J, R, 47, sd=sig, mean=0.0)
     s.set_model(*m.params())
     s.factor_epoch(0.01, 0.01)
     O.update_factor_epoch(m, t, 0.01, 0.01, O.Rng(1))
