@@ -20,6 +20,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sgdt_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -367,6 +369,10 @@ int core_launch_rp(Session& s, CoreArgs& a) {
     uint64_t rows = 0;
     for (int k = 0; k < s.order; ++k) rows += s.dims[k];
     if (rows > static_cast<uint64_t>(grid) * block * 8) grid = s.num_sms;
+  }
+  if (const char* e = std::getenv("SGDT_CORE_GRID")) {  // diagnostics (A/B runs)
+    const int g = std::atoi(e);
+    if (g >= 1 && g <= s.num_sms) grid = g;
   }
   a.cap = static_cast<uint32_t>((a.m + grid - 1) / grid);
   const size_t local = static_cast<size_t>(a.cap) * (a.js + RP + 2) * sizeof(float);
