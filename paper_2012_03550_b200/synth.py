@@ -23,7 +23,6 @@ No dataset is fetched or reproduced: Netflix/MovieLens/Yahoo are not here.
 from __future__ import annotations
 
 import dataclasses
-import math
 
 import numpy as np
 import torch
