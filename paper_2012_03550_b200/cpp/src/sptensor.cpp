@@ -8,6 +8,7 @@
 #include <limits>
 #include <numeric>
 #include <string>
+#include <thread>
 
 #include "device.hpp"
 
@@ -30,30 +31,69 @@ Shape::Shape(std::vector<std::uint32_t> dims) : dims_(std::move(dims)) {
 
 namespace {
 
+// Host threads for the O(nnz) construction work (a Netflix-sized tensor has
+// 10^8 entries; the reference builds it on one thread).
+unsigned ctor_threads(std::size_t nnz) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t by_size = std::max<std::size_t>(1, nnz / (1u << 20));
+  return static_cast<unsigned>(std::min<std::size_t>({hw, by_size, 64}));
+}
+
+template <class F>
+void parallel_for(unsigned nt, std::size_t n, F&& f) {  // f(begin, end) over nt slices
+  if (nt <= 1) {
+    f(std::size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+  f(std::size_t{0}, n / nt);
+  for (auto& th : pool) th.join();
+}
+
 // Duplicate detection: sort (128-bit linear position, entry id) pairs.  The
 // reference reports the first entry, in entry order, whose position was seen
 // before (sptensor.cpp:90-99): in every group of equal positions that is the
 // group's second-smallest id, and the answer is the smallest of those (or nnz
 // when there is none).  The reference's 64-bit key wraps for shapes beyond
-// 2^64 elements, hence the two-word key.
+// 2^64 elements, hence the two-word key.  Slices are sorted on host threads
+// and merged pairwise.
 std::size_t first_duplicate(const Shape& shape, const std::vector<std::uint32_t>& coords, std::size_t nnz) {
   const std::size_t order = shape.order();
   struct Key {
     std::uint64_t hi, lo;
     std::uint32_t e;
   };
-  std::vector<Key> keys(nnz);
-  for (std::size_t e = 0; e < nnz; ++e) {
-    unsigned __int128 key = 0, stride = 1;
-    for (std::size_t k = 0; k < order; ++k) {
-      key += static_cast<unsigned __int128>(coords[e * order + k] - 1) * stride;
-      stride *= shape.dim(k);
-    }
-    keys[e] = {static_cast<std::uint64_t>(key >> 64), static_cast<std::uint64_t>(key), static_cast<std::uint32_t>(e)};
-  }
-  std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+  auto less = [](const Key& a, const Key& b) {
     return a.hi != b.hi ? a.hi < b.hi : a.lo != b.lo ? a.lo < b.lo : a.e < b.e;
+  };
+  std::vector<Key> keys(nnz);
+  const unsigned nt = ctor_threads(nnz);
+  parallel_for(nt, nnz, [&](std::size_t b, std::size_t e) {
+    for (std::size_t i = b; i < e; ++i) {
+      unsigned __int128 key = 0, stride = 1;
+      for (std::size_t k = 0; k < order; ++k) {
+        key += static_cast<unsigned __int128>(coords[i * order + k] - 1) * stride;
+        stride *= shape.dim(k);
+      }
+      keys[i] = {static_cast<std::uint64_t>(key >> 64), static_cast<std::uint64_t>(key), static_cast<std::uint32_t>(i)};
+    }
+    std::sort(keys.begin() + static_cast<std::ptrdiff_t>(b), keys.begin() + static_cast<std::ptrdiff_t>(e), less);
   });
+  // pairwise merges of the sorted slices, a round of independent merges at a time
+  std::vector<std::size_t> cut(nt + 1);
+  for (unsigned t = 0; t <= nt; ++t) cut[t] = nnz * t / nt;
+  for (std::size_t width = 1; width < nt; width *= 2) {
+    std::vector<std::thread> pool;
+    for (std::size_t t = 0; t + width < nt; t += 2 * width) {
+      const std::size_t b = cut[t], m = cut[t + width], e = cut[std::min<std::size_t>(t + 2 * width, nt)];
+      pool.emplace_back([&, b, m, e] {
+        std::inplace_merge(keys.begin() + static_cast<std::ptrdiff_t>(b), keys.begin() + static_cast<std::ptrdiff_t>(m),
+                           keys.begin() + static_cast<std::ptrdiff_t>(e), less);
+      });
+    }
+    for (auto& th : pool) th.join();
+  }
   std::size_t first = nnz;
   for (std::size_t i = 1; i < nnz; ++i) {
     const bool same = keys[i].hi == keys[i - 1].hi && keys[i].lo == keys[i - 1].lo;
@@ -89,10 +129,11 @@ CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector
   if (bad_range < nnz) throw DataError("entry " + std::to_string(bad_range) + ": coordinate out of range");
 
   // Stable counting sort per mode: bucket i holds the entries with i_n = i in
-  // ascending entry id (the order the device mode copies inherit).
+  // ascending entry id (the order the device mode copies inherit); one host
+  // thread per mode.
   mode_perm_.assign(order, {});
   mode_offsets_.assign(order, {});
-  for (std::size_t n = 0; n < order; ++n) {
+  auto bucket_mode = [&](std::size_t n) {
     std::vector<std::uint64_t>& off = mode_offsets_[n];
     off.assign(static_cast<std::size_t>(shape_.dim(n)) + 1, 0);
     for (std::size_t e = 0; e < nnz; ++e) ++off[coords_[e * order + n]];
@@ -101,6 +142,14 @@ CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector
     std::vector<std::uint32_t>& perm = mode_perm_[n];
     perm.resize(nnz);
     for (std::size_t e = 0; e < nnz; ++e) perm[next[coords_[e * order + n] - 1]++] = static_cast<std::uint32_t>(e);
+  };
+  if (ctor_threads(nnz) > 1) {
+    std::vector<std::thread> pool;
+    for (std::size_t n = 1; n < order; ++n) pool.emplace_back(bucket_mode, n);
+    bucket_mode(0);
+    for (auto& th : pool) th.join();
+  } else {
+    for (std::size_t n = 0; n < order; ++n) bucket_mode(n);
   }
 }
 
