@@ -103,3 +103,21 @@ def test_training_reduces_rmse(c2):
     met = s.train(sgdt.CoreHyper(0.01, 0.01, 65536, 0, 0), sgdt.FactorHyper(0.01, 0.01, 1.0), 3)
     assert met[-1, 2] < r0 and met[-1, 2] <= met[0, 2] + 1e-9
     assert np.all(np.isfinite(met[:, 4]))
+
+
+def test_generated_config2_tensor_properties(c2):
+    """sgdt_synth at full size (the oracle restatement is checked at small
+    sizes in test_synth.py): distinct positions, ratings 1..5, the Zipf modes
+    hottest at index 1, and the 90/10 split sizes of train_test_split."""
+    dims = np.array(c2["dims"], np.int64)
+    trc, trv = c2["train"]
+    tec, tev = c2["test"]
+    assert len(trv) == 90_000_000 and len(tev) == 10_000_000
+    allc = np.concatenate([trc, tec]).astype(np.int64)
+    assert allc.min() >= 1 and np.all(allc.max(0) <= dims)
+    key = (allc[:, 0] - 1) + dims[0] * ((allc[:, 1] - 1) + dims[1] * (allc[:, 2] - 1))
+    assert len(np.unique(key)) == len(key)
+    assert set(np.unique(np.concatenate([trv, tev]))) <= {1.0, 2.0, 3.0, 4.0, 5.0}
+    for n in (0, 1):  # Zipf(1.1) modes: index 1 holds the most entries
+        counts = np.bincount(allc[:, n])
+        assert counts[1] == counts.max()
