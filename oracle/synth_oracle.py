@@ -141,3 +141,38 @@ def synth(dims, zipf, nnz: int, J: int, R: int, ratings: bool, noise: float, see
     else:
         v = x
     return coords, v
+
+
+# ---------------------------------------------------------------- host C++
+# oracle/synth_host.cpp: the same generator on all host threads, for sizes the
+# numpy restatement cannot reach (bench.py's reference arm builds the full
+# config tensor with it, without loading any product library).
+_host = None
+
+
+def _host_lib():
+    global _host
+    if _host is None:
+        import ctypes as C
+        import os
+        so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libsynth_host.so")
+        L = C.CDLL(so)
+        u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+        f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.sh_synth.argtypes = [C.c_int, u32p, f64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_double,
+                               C.c_uint64, C.c_int, u32p, f64p]
+        L.sh_synth.restype = C.c_int
+        _host = L
+    return _host
+
+
+def synth_host(dims, zipf, nnz: int, J: int, R: int, ratings: bool, noise: float, seed: int, threads: int = 0):
+    """Same result as synth() (and sgdt_synth), computed by synth_host.cpp."""
+    d = np.ascontiguousarray(dims, np.uint32)
+    z = np.ascontiguousarray(zipf, np.float64)
+    coords = np.empty((nnz, len(dims)), np.uint32)
+    values = np.empty(nnz, np.float64)
+    rc = _host_lib().sh_synth(len(dims), d, z, nnz, J, R, int(ratings), noise, seed, threads, coords, values)
+    if rc != 0:
+        raise ValueError(f"sh_synth failed with code {rc}")
+    return coords, values

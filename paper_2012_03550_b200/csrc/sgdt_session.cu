@@ -303,6 +303,118 @@ int check_coords(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, co
   return SGDT_OK;
 }
 
+// Duplicate detection (the CooTensor constructor's hash-set pass,
+// sptensor.cpp:90-100), as a sort: every entry's coordinates are packed into
+// a bit string of sum_k ceil(log2 I_k) bits (equal strings <=> equal
+// coordinates, no 2^64 limit), sorted least-significant word first by stable
+// radix sorts of (word, entry id) pairs, and each entry equal to its sorted
+// predecessor is a repeat.  The reference throws at the first entry id whose
+// key was seen before; ids ascend inside a group of equal keys (iota start,
+// stable passes), so that is the smallest id that is not first of its group.
+struct KeyLayout {
+  uint32_t shift[kMaxOrder];  // bit offset of mode k's field
+};
+__global__ void dup_key_word_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, int order, KeyLayout kl,
+                                    int word, const uint32_t* __restrict__ perm, uint64_t* __restrict__ keys) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nnz;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = perm[q];
+    uint64_t w = 0;
+    for (int k = 0; k < order; ++k) {
+      const uint64_t v = idx[static_cast<uint64_t>(k) * nnz + e];
+      const int lo = static_cast<int>(kl.shift[k]) - 64 * word;  // field start relative to this word
+      if (lo >= 0 && lo < 64) w |= v << lo;
+      else if (lo < 0 && lo > -32) w |= v >> (-lo);
+    }
+    keys[q] = w;
+  }
+}
+
+__global__ void dup_adjacent_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, int order,
+                                    const uint32_t* __restrict__ perm, unsigned long long* first_dup) {
+  for (uint64_t q = 1 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nnz;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t a = perm[q - 1], b = perm[q];
+    bool eq = true;
+    for (int k = 0; k < order && eq; ++k)
+      eq = idx[static_cast<uint64_t>(k) * nnz + a] == idx[static_cast<uint64_t>(k) * nnz + b];
+    if (eq) atomicMin(first_dup, static_cast<unsigned long long>(b));
+  }
+}
+
+int check_duplicates(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, const char* what) {
+  const uint64_t nnz = rc.nnz;
+  if (nnz < 2) return SGDT_OK;
+  KeyLayout kl{};
+  uint32_t total = 0;
+  for (int k = 0; k < d->order; ++k) {
+    kl.shift[k] = total;
+    uint32_t b = 0;
+    while (b < 32 && (1ull << b) < d->dims[k]) ++b;
+    total += b;
+  }
+  const int words = std::max<int>(1, static_cast<int>((total + 63) / 64));
+  uint64_t *k_in = nullptr, *k_out = nullptr;
+  uint32_t *p_in = nullptr, *p_out = nullptr;
+  unsigned long long* first = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  unsigned long long h = ~0ull;
+  int rc_ = SGDT_OK;
+  do {
+    if ((rc_ = dalloc(&k_in, nnz)) || (rc_ = dalloc(&k_out, nnz)) || (rc_ = dalloc(&p_in, nnz)) ||
+        (rc_ = dalloc(&p_out, nnz)) || (rc_ = dalloc(&first, 1)))
+      break;
+    iota_u32_kernel<<<grid_for(nnz, s.num_sms), 256, 0, s.stream>>>(p_in, nnz);
+    for (int w = 0; w < words && rc_ == SGDT_OK; ++w) {
+      const int bits = std::max<int>(1, std::min<int>(64, static_cast<int>(total) - 64 * w));
+      dup_key_word_kernel<<<grid_for(nnz, s.num_sms), 256, 0, s.stream>>>(rc.idx, nnz, d->order, kl, w, p_in,
+                                                                          k_in);
+      size_t need = 0;
+      if (cub::DeviceRadixSort::SortPairs(nullptr, need, k_in, k_out, p_in, p_out, static_cast<int64_t>(nnz), 0,
+                                          bits, s.stream) != cudaSuccess) {
+        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check (sort sizing) failed");
+        break;
+      }
+      if (need > tmp_bytes) {
+        if (tmp) cudaFree(tmp);
+        tmp = nullptr;
+        if (cudaMalloc(&tmp, need) != cudaSuccess) {
+          cudaGetLastError();
+          rc_ = fail(SGDT_ERR_CONFIG, std::string(what) + ": out of device memory in the duplicate check");
+          break;
+        }
+        tmp_bytes = need;
+      }
+      if (cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, p_in, p_out, static_cast<int64_t>(nnz), 0,
+                                          bits, s.stream) != cudaSuccess) {
+        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check (sort) failed");
+        break;
+      }
+      std::swap(p_in, p_out);
+    }
+    if (rc_) break;
+    if (cudaMemcpyAsync(first, &h, sizeof h, cudaMemcpyHostToDevice, s.stream) != cudaSuccess) {
+      rc_ = fail(SGDT_ERR_INTERNAL, "duplicate check: copy failed");
+      break;
+    }
+    dup_adjacent_kernel<<<grid_for(nnz, s.num_sms), 256, 0, s.stream>>>(rc.idx, nnz, d->order, p_in, first);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(&h, first, sizeof h, cudaMemcpyDeviceToHost, s.stream) != cudaSuccess ||
+        cudaStreamSynchronize(s.stream) != cudaSuccess) {
+      cudaGetLastError();
+      rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check failed");
+    }
+    s.launches += 2 + words;
+  } while (false);
+  for (void* p : {(void*)k_in, (void*)k_out, (void*)p_in, (void*)p_out, (void*)first, tmp})
+    if (p) cudaFree(p);
+  if (rc_) return rc_;
+  if (h != ~0ull)
+    return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(h) + ": duplicate coordinate");
+  return SGDT_OK;
+}
+
 // The whole mode-n order and its row offsets on the device (CooTensor::
 // mode_perm / mode_offsets, sptensor.cpp:102-117, built by a stable radix sort
 // instead of the host counting sort): rows ascending by i_n; inside a row by
@@ -800,6 +912,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     // records: entry order (kept for Psi gathers + train RMSE) and per mode
     TRY(upload_record_copy(*s, train, s->train_rec, nullptr, nullptr));
     TRY(check_coords(*s, s->train_rec, train, "train"));
+    TRY(check_duplicates(*s, s->train_rec, train, "train"));
     uint32_t max_pieces = 0;
     std::vector<uint64_t> off;
     std::vector<uint32_t> perm;
@@ -866,6 +979,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
       s->nnz_test = test->nnz;
       TRY(upload_record_copy(*s, test, s->test_rec, nullptr, nullptr));
       TRY(check_coords(*s, s->test_rec, test, "test"));
+      TRY(check_duplicates(*s, s->test_rec, test, "test"));
     }
     // model
     uint64_t stage = 0;

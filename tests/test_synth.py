@@ -60,3 +60,45 @@ def test_device_generator_errors():
         sgdt.synth((10, 10), (0.0, 0.0), 60, 2, 2, False, 0.0, 1)  # more than half the index space
     with pytest.raises(Exception):
         sgdt.synth((10,), (0.0,), 3, 2, 2, False, 0.0, 1)  # order 1
+
+
+_NUMPY_CACHE = {}
+
+
+def _numpy_synth(args):
+    if args not in _NUMPY_CACHE:
+        _NUMPY_CACHE[args] = S.synth(*args)
+    return _NUMPY_CACHE[args]
+
+
+@pytest.mark.parametrize("spec", SPECS, ids=[str(i) for i in range(len(SPECS))])
+@pytest.mark.parametrize("threads", [1, 5])
+def test_host_generator_matches_oracle(spec, threads):
+    """oracle/synth_host.cpp (the bench reference arm's input generator) against
+    the numpy restatement: indices bit-exact, values to fp64 rounding."""
+    args = (spec["dims"], spec["zipf"], spec["nnz"], spec["J"], spec["R"], spec["ratings"], spec["noise"],
+            spec["seed"])
+    c, v = S.synth_host(*args, threads=threads)
+    rc, rv = _numpy_synth(args)
+    assert np.array_equal(c, rc)
+    assert np.allclose(v, rv, rtol=1e-12, atol=1e-12)
+
+
+def test_host_generator_errors():
+    with pytest.raises(ValueError):
+        S.synth_host((10, 10), (0.0, 0.0), 60, 2, 2, False, 0.0, 1)
+    with pytest.raises(ValueError):
+        S.synth_host((10, 10), (-1.0, 0.0), 5, 2, 2, False, 0.0, 1)
+
+
+@pytest.mark.gpu
+def test_host_generator_matches_device_at_scale():
+    """A config-2-shaped tensor of 3M entries: host and device generators give
+    the same positions in the same order (the reference arm trains on the
+    host one, the GPU arm on the device one)."""
+    from paper_2012_03550_b200 import sgdt
+    args = ((48000, 1780, 2200), (1.1, 1.1, 0.0), 3_000_000, 10, 10, True, 0.0, 1)
+    c, v = sgdt.synth(*args, device=0)
+    hc, hv = S.synth_host(*args)
+    assert np.array_equal(c, hc)
+    assert np.mean(v != hv) < 1e-4  # ratings: a rounding tie may flip in a rare entry
