@@ -6,20 +6,30 @@ units / (core_s + factor_s), RMSE evaluation excluded (trainer.cpp:94-107).
 A "step" is one training epoch (core phase + factor phase) over the resident
 training tensor.
 
-Workload: BASELINE config 2 (configs[1]) -- 480,000 x 17,800 x 2,200, 100M
-nonzeros, Zipf(1.1) on modes 1-2, uniform mode 3, integer 1-5 ratings from a
-planted rank-10 teacher, 90/10 split, J = R = 10, M = 65,536 -- generated
-synthetically (paper_2012_03550_b200/synth.py); Netflix itself is not here.
+Workload (default): BASELINE config 3 (configs[2]), the largest configuration
+that runs on one GPU -- 1,000,000 x 1,000,000 x 100,000 x 50, 500M nonzeros,
+Zipf(1.05) on modes 1-3, uniform mode 4, planted J_n = R_core = 8 teacher plus
+N(0, 0.05^2) noise, 90/10 split (450M training nonzeros), J = R = 8,
+M = 262,144.  --config 2|4|5 selects the others.  The tensor is synthetic
+(SURVEY.md 8(d) generator): the GPU arm draws it on the device
+(paper_2012_03550_b200/synth.py -> sgdt_synth), the reference arm draws the
+identical tensor on the host (oracle/synth_host.cpp) so that it never loads a
+product library or touches the GPU.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the reference's own CPU implementation (oracle/_ref,
-the unmodified reference sources compiled in place; else the C oracle port) on
-a bounded sample of the same workload with every host thread.
+--impl reference runs the reference's own CPU implementation (oracle/_ref: the
+unmodified reference sources compiled in place) on the SAME full training
+tensor, Strategy::Improved on every host thread, through its timed_epochs loop
+(eval.cpp:201-223).  One config 3 epoch takes minutes on the CPU, so the epoch
+counts are capped by a wall-clock budget (--ref-budget); the line states how
+many epochs were timed and how many were asked for.
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import os
 import statistics
@@ -34,7 +44,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
-CPU_SAMPLE_NNZ = 3_000_000
 
 
 def parse():
@@ -43,26 +52,31 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
+    p.add_argument("--config", type=int, default=3, choices=[2, 3, 4, 5])
     p.add_argument("--scale", type=float, default=1.0,
                    help="fraction of the config's nnz (debug only; 1.0 for reported runs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="override the per-config CPU sample size")
+    p.add_argument("--ref-budget", type=float, default=150.0,
+                   help="wall-clock seconds of reference epochs (--impl reference)")
     p.add_argument("--row-fraction", type=float, default=1.0,
                    help="FactorHyper::row_fraction of our arm (diagnostics; the headline uses 1.0)")
     p.add_argument("--sharded", action="store_true",
-                   help="use the multi-GPU (sharded factor phase) driver even on one rank")
+                   help="use the multi-GPU (sharded) driver even on one rank")
+    p.add_argument("--core", choices=["replicated", "sharded"], default="replicated",
+                   help="multi-GPU core phase: Psi slices + peer-reduced partials, or replicated")
     return p.parse_args()
 
 
-HYPER = dict(lr_a=0.01, lr_b=0.01, reg_a=0.01, reg_b=0.01, init_mean=0.5, init_sd=0.1, seed=1)
+HYPER = dict(lr_a=0.01, lr_b=0.01, reg_a=0.01, reg_b=0.01, seed=1)
 BATCH_M = {2: 65536, 3: 262144, 4: 65536, 5: 262144}
-# CPU-baseline sample per config (nonzeros): the reference's per-unit cost is
-# prod(J) FMAs (dense core), so large cores get smaller samples.
-CPU_SAMPLE = {2: 3_000_000, 3: 2_000_000, 4: 0, 5: 100_000}
+# cpu_baseline sample of our arm (nonzeros; a bounded 10-30 s leg): the
+# reference's per-unit cost is prod(J) FMAs (dense core).
+CPU_SAMPLE = {2: 3_000_000, 3: 4_000_000, 4: 0, 5: 100_000}
 REF_UNAVAILABLE = {4: "the reference rejects config 4: Shape overflows 64 bits (1e5^4 x 1e3, sptensor.cpp:34-35) "
                       "and prod J = 16^5 exceeds kMaxCoreElems (model.hpp:25)"}
+L2_NOTE = "inputs larger than L2: the COO record copies (N+1 copies x 4(N+1) B x nnz) exceed the 126 MB L2"
 
 
 def init_stats(cfg, spec):
@@ -72,8 +86,44 @@ def init_stats(cfg, spec):
     converges for every seed tried).  Configs 3-5 use N(0, sigma^2) at the
     teacher's unit-variance scale."""
     if cfg == 2:
-        return 0.3, HYPER["init_sd"]
+        return 0.3, 0.1
     return 0.0, spec.unit_sigma
+
+
+def config_spec(cfg, scale):
+    from paper_2012_03550_b200 import synth  # pure Python (no library load)
+    spec = synth.CONFIGS[cfg]
+    if scale != 1.0:
+        spec = synth.scaled(spec, scale ** (1.0 / len(spec.dims)), int(spec.nnz * scale))
+    return spec
+
+
+def units_per_epoch(order, m, nnz):
+    return order * (m + nnz)
+
+
+def bytes_per_unit(order, R):
+    """B_u = 4(N+1) + 4(N-1)R: one u32/fp32 COO record + N-1 gathered rows of R fp32."""
+    return 4 * (order + 1) + 4 * (order - 1) * R
+
+
+def n_train(nnz, test_fraction=0.1):
+    return nnz - int(round(test_fraction * nnz))
+
+
+def workload(cfg, spec, m, row_fraction):
+    """The `config` object of the JSON line -- identical in both arms."""
+    order = len(spec.dims)
+    J = R = spec.teacher_j
+    nt = n_train(spec.nnz, spec.test_fraction)
+    mean, sd = init_stats(cfg, spec)
+    units = units_per_epoch(order, m, nt) if row_fraction == 1.0 else int(order * (m + row_fraction * nt))
+    return {"workload": f"config{cfg}", "dims": list(spec.dims), "zipf": list(spec.zipf),
+            "values": "ratings 1-5" if spec.values == "ratings" else f"teacher + N(0, {spec.noise}^2)",
+            "nnz_total": spec.nnz, "nnz_train": nt, "split": "90/10 train_test_split, Rng(seed + 7)",
+            "J": J, "R": R, "batch_m": m, "row_fraction": row_fraction, "units_per_step": units,
+            "lr": HYPER["lr_a"], "reg": HYPER["reg_a"], "init": f"N({mean:.4g}, {sd:.4g}^2)", "seed": HYPER["seed"],
+            "l2": L2_NOTE}
 
 
 def measured_peak():
@@ -83,6 +133,34 @@ def measured_peak():
         return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def build_id():
+    """Hash of the CUDA sources and the C-ABI header: stamps the ncu traffic
+    file so the bench only reports traffic measured on this build."""
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2012_03550_b200", "csrc", "*.cu*"))) + \
+        [os.path.join(ROOT, "include", "sgdt.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    return model, cores
 
 
 class ClockSampler:
@@ -133,23 +211,11 @@ class ClockSampler:
 
 
 def make_data(cfg: int, scale: float, device):
-    import torch
     from paper_2012_03550_b200 import synth
-    spec = synth.CONFIGS[cfg]
-    if scale != 1.0:
-        spec = synth.scaled(spec, scale ** (1.0 / len(spec.dims)), int(spec.nnz * scale))
+    spec = config_spec(cfg, scale)
     t0 = time.time()
     train, test, _ = synth.generate(spec, device)
     return dict(spec=spec, train=train, test=test, gen_s=time.time() - t0)
-
-
-def units_per_epoch(order, m, nnz):
-    return order * (m + nnz)
-
-
-def bytes_per_unit(order, R):
-    """B_u = 4(N+1) + 4(N-1)R: one u32/fp32 COO record + N-1 gathered rows of R fp32."""
-    return 4 * (order + 1) + 4 * (order - 1) * R
 
 
 def init_model(dims, J, R, mean, sd, seed):
@@ -159,84 +225,128 @@ def init_model(dims, J, R, mean, sd, seed):
     return A, B
 
 
-def cpu_reference_run(data, J, R, m, warmup, epochs, threads, init=(0.5, 0.1)):
-    """Reference CPU epochs on a bounded sample of the same tensor.
-    Returns (seconds/epoch, kind, cores, sample_desc, units/epoch)."""
+def cpu_sample_run(cfg, spec, trc, trv, m, sample, threads):
+    """Our arm's cpu_baseline: the reference (oracle/_ref) on a bounded uniform
+    subsample of the training tensor, 1 timed epoch after 1 warm-up."""
     from oracle import oracle_py as O
-    spec = data["spec"]
-    trc, trv = data["train"]
+    import ctypes as C
     rs = np.random.default_rng(12345)
-    S = min(len(trv), data.get("cpu_sample") or CPU_SAMPLE.get(data["cfg"], CPU_SAMPLE_NNZ))
+    S = min(len(trv), sample)
     pick = np.sort(rs.choice(len(trv), S, replace=False))
-    c, v = trc[pick], trv[pick]
     order = len(spec.dims)
+    J = R = spec.teacher_j
     mm = min(m, S)
     Jv = np.array([J] * order, np.uint32)
-    desc = (f"{S:,} of {len(trv):,} training nonzeros of config {data['cfg']} (uniform random "
-            f"subset, same shape), M={mm}, {epochs} timed epoch(s) after {warmup} warm-up, "
-            f"Strategy::Improved, init N({init[0]:.3g},{init[1]:.3g}^2)")
-    if O.ref_available():
-        import ctypes as C
-        t = O.RefTensor(spec.dims, c, v)
-        sec = C.c_double()
-        rc = O.ref().ref_time_epochs(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"], mm, 2, threads,
-                                     warmup, epochs, 1, init[0], init[1], C.byref(sec))
-        if rc != 0:
-            raise RuntimeError(f"reference bench failed: {rc}")
-        return sec.value, "reference", threads, desc, units_per_epoch(order, mm, S)
-    # oracle port: single thread, serial strategy
-    t = O.Tensor(spec.dims, c, v)
-    model = O.Model(spec.dims, Jv, R).init_gaussian(init[0], init[1], 1)
-    rng = O.Rng(2)
-    ws = O.CoreWorkspace(S)
-    times = []
-    for e in range(warmup + epochs):
-        t0 = time.perf_counter()
-        O.update_core_epoch(model, t, HYPER["lr_b"], HYPER["reg_b"], mm, rng, ws)
-        O.update_factor_epoch(model, t, HYPER["lr_a"], HYPER["reg_a"], rng)
-        if e >= warmup:
-            times.append(time.perf_counter() - t0)
-    return statistics.median(times), "port", 1, desc.replace("Strategy::Improved", "serial C port"), \
-        units_per_epoch(order, mm, S)
+    model, cores = cpu_info()
+    desc = (f"{S:,} of {len(trv):,} training nonzeros of config {cfg} (uniform random subset, same shape), "
+            f"M={mm}, 1 timed epoch after 1 warm-up, Strategy::Improved, {threads} threads, {model}")
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref is not built")
+    t = O.RefTensor(spec.dims, trc[pick], trv[pick])
+    sec = C.c_double()
+    mean, sd = init_stats(cfg, spec)
+    rc = O.ref().ref_time_epochs(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"], mm, 2, threads,
+                                 1, 1, HYPER["seed"], mean, sd, C.byref(sec))
+    if rc != 0:
+        raise RuntimeError(f"reference epoch failed: {rc}")
+    return {"value": units_per_epoch(order, mm, S) / sec.value, "unit": "updates/s", "cores": threads,
+            "kind": "reference", "sample": desc, "cpu_model": model}
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU implementation on the same full tensor.  Loads
+    only oracle/ libraries (host generator, host split, the compiled
+    reference); never imports torch or touches the GPU."""
     if rank != 0:
         return 0
-    if args.config in REF_UNAVAILABLE:
-        print(json.dumps({"impl": "reference", "unavailable": REF_UNAVAILABLE[args.config]}), flush=True)
-        return 0
-    import torch
     cfg = args.config
-    data = make_data(cfg, args.scale, "cuda" if torch.cuda.is_available() else "cpu")
-    data["cfg"] = cfg
-    data["cpu_sample"] = args.cpu_sample
-    spec = data["spec"]
-    threads = os.cpu_count() or 1
+    if cfg in REF_UNAVAILABLE:
+        print(json.dumps({"impl": "reference", "unavailable": REF_UNAVAILABLE[cfg]}), flush=True)
+        return 0
+    import ctypes as C
+    from oracle import oracle_py as O
+    from oracle import synth_oracle as S
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the compiled reference) is not built"}),
+              flush=True)
+        return 0
+    spec = config_spec(cfg, args.scale)
+    order = len(spec.dims)
     J = R = spec.teacher_j
     m = BATCH_M[cfg]
-    sec, kind, cores, desc, units = cpu_reference_run(data, J, R, m, args.warmup, args.steps, threads,
-                                                      init_stats(cfg, spec))
-    value = units / sec
+    model_name, threads = cpu_info()
+    t0 = time.time()
+    coords, values = S.synth_host(spec.dims, spec.zipf, spec.nnz, spec.teacher_j, spec.teacher_r,
+                                  spec.values == "ratings", spec.noise, spec.seed, threads)
+    t1 = time.time()
+    _, tr = S.split_ids_host(spec.nnz, spec.test_fraction, spec.seed + 7)
+    trc, trv = coords[tr], values[tr]
+    del coords, values, tr
+    t2 = time.time()
+    t = O.RefTensor(spec.dims, trc, trv)  # the reference CooTensor constructor
+    del trc, trv
+    t3 = time.time()
+    Jv = np.array([J] * order, np.uint32)
+    secs = np.zeros(max(args.steps, 1))
+    nw, nt = C.c_size_t(), C.c_size_t()
+    mean, sd = init_stats(cfg, spec)
+    rc = O.ref().ref_time_epochs_budget(t.h, Jv, R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"], m, 2, threads,
+                                        args.warmup, max(args.steps, 1), HYPER["seed"], mean, sd, args.ref_budget,
+                                        secs, C.byref(nw), C.byref(nt))
+    if rc != 0:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference epochs failed with code {rc}"}), flush=True)
+        return 0
+    timed = secs[:nt.value]
+    med = float(np.median(timed))
+    cfgd = workload(cfg, spec, m, 1.0)
+    value = cfgd["units_per_step"] / med
+    sample = (f"the full config {cfg} training tensor ({cfgd['nnz_train']:,} nonzeros, generated on the host by "
+              f"oracle/synth_host.cpp, identical to the device generator's); timed_epochs loop (eval.cpp:201-223), "
+              f"Strategy::Improved, {threads} threads on {model_name}; median of {nt.value} timed epoch(s) after "
+              f"{nw.value} warm-up (asked: {args.steps} after {args.warmup}; capped by a {args.ref_budget:.0f} s "
+              f"budget, one epoch takes {timed[0]:.1f} s)")
     line = {
-        "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
-        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "gpu_launches": 0,
-        "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz": spec.nnz, "J": J, "R": R,
-                   "batch_m": m, "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind, "sample": desc},
+        "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": int(nt.value), "warmup": int(nw.value), "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
+        "gpu_launches": 0, "config": cfgd,
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "reference",
+                         "sample": sample, "cpu_model": model_name},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "run": {"epoch_s": [float(x) for x in timed], "data_gen_s": t1 - t0, "split_s": t2 - t1,
+                "tensor_build_s": t3 - t2},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def factor_traffic(cfg, mode_ms, peak):
+    """ncu DRAM / L2 bytes per factor-mode launch group of THIS build
+    (profiles/factor_traffic.json, written by scripts/ncu_factor_traffic.py,
+    stamped with build_id()).  None when the file is for another build."""
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "factor_traffic.json")))
+    except Exception:
+        return None
+    if tj.get("build") != build_id():
+        return {"stale": f"profiles/factor_traffic.json is for build {tj.get('build')}, this is {build_id()}"}
+    c = tj.get(f"config{cfg}")
+    if not c:
+        return None
+    dram = c["dram_bytes_per_mode"]
+    avg_ms = sum(mode_ms) / len(mode_ms)
+    return {"dram_bytes": dram, "l2_bytes": c.get("l2_bytes_per_mode"),
+            "dram_gbs": dram / (avg_ms * 1e-3) / 1e9, "dram_frac": dram / (avg_ms * 1e-3) / 1e9 / peak,
+            "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum (build {tj['build']})"}
+
+
 def run_sharded(args, rank, world, local_rank):
     """N GPUs: factor phase sharded over ranks (partition_even slices of every
-    mode order, rank-ordered boundary merge, NCCL row-block broadcast), core
-    phase replicated -- paper_2012_03550_b200/distributed.py.  Total work is
-    the config's epoch, so scaling is strong."""
+    mode order, peer-published rows, rank-ordered boundary merge), core phase
+    sharded (partition_even Psi slices, rank-ordered peer-reduced column
+    partials) or replicated -- paper_2012_03550_b200/distributed.py.  Total
+    work is the config's epoch, so scaling is strong."""
     import torch
     import torch.distributed as dist
     from paper_2012_03550_b200 import distributed as D
@@ -267,7 +377,7 @@ def run_sharded(args, rank, world, local_rank):
     s.seed(HYPER["seed"] + 1)
     ch = sgdt.CoreHyper(HYPER["lr_b"], HYPER["reg_b"], m, 0, 0)
     fh = sgdt.FactorHyper(HYPER["lr_a"], HYPER["reg_a"], 1.0)
-    D.connect_peers(s, group)  # peer-store publication (IPC-mapped peers over NVLink)
+    D.connect_peers(s, group)
     dist.barrier()
     D.run_epochs_p2p(s, group, ch, fh, args.warmup)
     stream = torch.cuda.ExternalStream(s.stream)
@@ -288,8 +398,6 @@ def run_sharded(args, rank, world, local_rank):
     elapsed_ms = float(t.item())
     units = units_per_epoch(order, m, nnz)
     value = units * args.steps / (elapsed_ms * 1e-3)
-    # end to end through the public API with host buffers on every rank:
-    # H2D of the fp64 model, the sharded epoch, D2H of the fp64 model
     e2e = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
@@ -322,17 +430,17 @@ def run_sharded(args, rank, world, local_rank):
                "path": "per rank: sgdt_set_model (fp64 pinned host) + sharded epoch + sgdt_get_model (fp64 pinned host)"}
     rmse = s.eval(1)[0]
     if rank == 0:
+        cfgd = workload(cfg, spec, m, 1.0)
         line = {
             "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
-            "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz_train": nnz, "J": J, "R": R,
-                       "batch_m": m, "units_per_step": units,
-                       "parallelism": f"factor phase sharded over {world} GPUs (partition_even slices; finalised "
-                                      "rows stored into every peer's A/Q over NVLink P2P, rank-ordered boundary "
-                                      "merge from peer-stored records, NCCL stream barriers); core phase replicated",
-                       "test_rmse_after": rmse, "setup_s": setup_s},
+            "config": cfgd,
+            "run": {"parallelism": f"{world} GPUs: factor phase sharded (partition_even slices of every mode "
+                                   "order; finalised rows stored into every peer's A/Q over NVLink P2P; rank-ordered "
+                                   f"boundary merge); core phase {args.core}",
+                    "test_rmse_after": rmse, "setup_s": setup_s, "data_gen_s": data["gen_s"]},
             "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
@@ -346,11 +454,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 or args.sharded:
         return run_sharded(args, rank, world, local_rank)
     torch.cuda.set_device(local_rank)
-    dist = None
     cfg = args.config
     data = make_data(cfg, args.scale, torch.device("cuda", local_rank))
-    data["cfg"] = cfg
-    data["cpu_sample"] = args.cpu_sample
     spec = data["spec"]
     order = len(spec.dims)
     J = R = spec.teacher_j
@@ -359,8 +464,7 @@ def run_ours(args, rank, world, local_rank):
     nnz = len(trv)
 
     t0 = time.time()
-    s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"],
-                     device=local_rank)
+    s = sgdt.Session(spec.dims, trc, trv, [J] * order, R, test=data["test"], device=local_rank)
     setup_s = time.time() - t0
     A, B = init_model(spec.dims, J, R, *init_stats(cfg, spec), HYPER["seed"])
     s.set_model(A, B)
@@ -373,8 +477,6 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.ExternalStream(s.stream)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
     torch.cuda.synchronize()
     launches0 = s.launch_count()
     with ClockSampler(local_rank) as clk:
@@ -383,34 +485,20 @@ def run_ours(args, rank, world, local_rank):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = s.launch_count() - launches0
-    if dist:
-        dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([elapsed_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-    timing = s.last_timing()
-    # N (M + f nnz); f < 1 keeps max(1, llround(f |bucket|)) per row,
-    # f nnz is its nominal size
-    units = units_per_epoch(order, m, nnz) if args.row_fraction == 1.0 else int(order * (m + args.row_fraction * nnz))
-    value = units * args.steps * world / (elapsed_ms * 1e-3)
+    timing = s.last_timing()  # per-phase means over the K timed epochs (CUDA events, session stream)
+    cfgd = workload(cfg, spec, m, args.row_fraction)
+    units = cfgd["units_per_step"]
+    value = units * args.steps / (elapsed_ms * 1e-3)
     ms_per_step = elapsed_ms / args.steps
 
-    # roofline of the dominant kernel (factor phase, one launch per mode)
+    # roofline of the dominant kernel: the factor phase's launches of one mode
     bu = bytes_per_unit(order, R)
     mode_ms = [timing.factor_mode_ms[n] for n in range(order)]
     avg_mode_ms = sum(mode_ms) / order
     achieved_gbs = nnz * bu / (avg_mode_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = l2_traffic = None
-    tpath = os.path.join(ROOT, "profiles", "factor_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            traffic, l2_traffic = tj.get(f"config{cfg}"), tj.get(f"config{cfg}_l2")
-        except Exception:
-            traffic = l2_traffic = None
+    traffic = factor_traffic(cfg, mode_ms, peak)
     # bytes outside B_u, per epoch: the mode-n row traffic of the
     # factor phase (read a and Q^(n), write a and Q^(n) per non-empty row) and
     # the Q^(k) refresh at the end of the core phase
@@ -447,49 +535,48 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.steps
-        e2e = {"value": units * world / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
+        e2e = {"value": units / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "sgdt_run_epochs_host(1): fp64 pinned host model in -> epoch -> fp64 pinned host model out",
-               "setup_s": setup_s}
+               "path": "sgdt_run_epochs_host(1): fp64 pinned host model in -> epoch -> fp64 pinned host model out"}
 
     cpu = None
     if rank == 0 and cfg in REF_UNAVAILABLE and not args.no_cpu_baseline:
         cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable", "sample": REF_UNAVAILABLE[cfg]}
     elif rank == 0 and not args.no_cpu_baseline:
         try:
-            sec, kind, cores, desc, cu = cpu_reference_run(data, J, R, m, 1, 1, os.cpu_count() or 1,
-                                                           init_stats(cfg, spec))
-            cpu = {"value": cu / sec, "unit": "updates/s", "cores": cores, "kind": kind, "sample": desc}
+            cpu = cpu_sample_run(cfg, spec, trc, trv, m, args.cpu_sample or CPU_SAMPLE[cfg], cpu_info()[1])
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",
                    "sample": f"{type(exc).__name__}: {exc}"}
 
-    if rank == 0:
-        line = {
-            "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
-            "config": {"workload": f"config{cfg}", "dims": list(spec.dims), "nnz_total": spec.nnz,
-                       "nnz_train": nnz, "J": J, "R": R, "batch_m": m, "row_fraction": args.row_fraction, "units_per_step": units,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "COO record copies (4 x 16 B x nnz) exceed the 126 MB L2; Q tables are L2-resident by design",
-                       "test_rmse_after": rmse, "data_gen_s": data["gen_s"], "setup_s": setup_s},
-            "phase_ms": {"core": timing.core_ms, "factor": timing.factor_ms, "factor_modes": mode_ms},
-            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": achieved_gbs / peak, "traffic": traffic, "l2_traffic": l2_traffic,
-                         "kernel": ("factor_staged_kernel / factor_chunk_kernel" if (R + 3) // 4 * 4 <= 12
-                                    else "factor_group_kernel") + " + factor_split_kernel (one mode)",
-                         "bytes_per_unit": bu, "units_per_launch": nnz, "peak_source": peak_src,
-                         "overhead_bytes_per_epoch": overhead},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
+            "traffic": traffic.get("dram_bytes") if traffic else None,
+            "frac_basis": "algorithmic: B_u x nnz per factor-mode launch group / its mean CUDA-event time; the "
+                          "gathered Q rows are served from L1/L2, so this can exceed 1 -- dram_frac is the HBM share",
+            "kernel": ("factor_staged_kernel / factor_chunk_kernel" if (R + 3) // 4 * 4 <= 12
+                       else "factor_group_kernel") + " + factor_split_kernel (one mode)",
+            "bytes_per_unit": bu, "units_per_launch": nnz, "launch_ms": avg_mode_ms,
+            "timed_epochs": int(timing.epochs), "peak_source": peak_src, "overhead_bytes_per_epoch": overhead}
+    if traffic:
+        roof.update({k: traffic[k] for k in ("dram_gbs", "dram_frac", "l2_bytes", "source") if k in traffic})
+        if "stale" in traffic:
+            roof["traffic_note"] = traffic["stale"]
+    line = {
+        "metric": "sampled-nnz SGD updates/sec", "value": value, "unit": "updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Zipf/uniform indices, planted teacher; no dataset)",
+        "config": cfgd,
+        "run": {"parallelism": "single GPU", "test_rmse_after": rmse, "data_gen_s": data["gen_s"],
+                "setup_s": setup_s, "build": build_id()},
+        "phase_ms": {"core": timing.core_ms, "factor": timing.factor_ms, "factor_modes": mode_ms},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -87,12 +87,15 @@ typedef struct {
   double max_imbalance;
 } sgdt_factor_stats;
 
-/* Per-phase device times of the last epoch run, from CUDA events. */
+/* Per-phase device times from CUDA events on the session stream: the means
+ * over the epochs of the last sgdt_run_epochs / sgdt_run_epochs_host /
+ * sgdt_train call (its last 1024 epochs at most; `epochs` says how many). */
 typedef struct {
   float sample_ms;
   float core_ms;
   float factor_ms;
   float factor_mode_ms[SGDT_MAX_ORDER];
+  uint32_t epochs;
 } sgdt_timing;
 
 const char* sgdt_last_error(void);

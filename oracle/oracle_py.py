@@ -374,6 +374,10 @@ def ref():
         L.ref_time_epochs.argtypes = [vp, u32p, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_size_t,
                                       C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, C.c_double,
                                       C.c_double, C.POINTER(C.c_double)]
+        L.ref_time_epochs_budget.argtypes = [vp, u32p, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                             C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64,
+                                             C.c_double, C.c_double, C.c_double, f64p, C.POINTER(C.c_size_t),
+                                             C.POINTER(C.c_size_t)]
         _ref = L
     return _ref
 

@@ -369,6 +369,56 @@ int ref_time_epochs(void* train_t, const std::uint32_t* J, std::uint32_t R, doub
   });
 }
 
+// timed_epochs (eval.cpp:201-223) under a wall-clock budget, for the bench's
+// reference arm on full-size tensors (one config 3 epoch takes minutes on
+// the CPU): the same model init, RNG seeding, workspaces and per-epoch
+// (core + factor) timing, but the epoch counts are capped so the run ends
+// in about budget_s.  The first epoch is a warm-up when warmup > 0 and two
+// epochs fit the budget; otherwise it is the (only) timed epoch.  Then up to
+// warmup - 1 more warm-ups and `epochs` timed epochs, as many as fit
+// (at least one timed).  secs_out receives every timed epoch (<= epochs).
+int ref_time_epochs_budget(void* train_t, const std::uint32_t* J, std::uint32_t R, double lr_a, double lr_b,
+                           double reg, std::size_t batch_m, int strategy, std::size_t threads, std::size_t warmup,
+                           std::size_t epochs, std::uint64_t seed, double init_mean, double init_sd,
+                           double budget_s, double* secs_out, std::size_t* n_warm, std::size_t* n_timed) {
+  GUARD({
+    const CooTensor& tr = *static_cast<RefTensor*>(train_t)->t;
+    TuckerModel model = TuckerModel::init_gaussian(
+        tr.shape(), Ranks{std::vector<std::uint32_t>(J, J + tr.order()), R}, init_mean, init_sd, seed);
+    Rng rng(seed + 1);
+    WorkerPool pool(threads);
+    SchedContext sched{threads <= 1 ? Strategy::Serial : strat_of(strategy), BalancePolicy::Dynamic,
+                       threads <= 1 ? nullptr : &pool};
+    CoreBatchWorkspace cws;
+    std::vector<RowBatchWorkspace> rws(sched.workers());
+    auto epoch = [&] {
+      const auto t0 = std::chrono::steady_clock::now();
+      update_core_epoch(model, tr, CoreHyper{lr_b, reg, batch_m, false, false}, sched, rng, cws);
+      update_factor_epoch(model, tr, FactorHyper{lr_a, reg, 1.0}, sched, rng, rws);
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    *n_warm = *n_timed = 0;
+    if (epochs == 0) return 0;
+    const double t1 = epoch();
+    double used = t1;
+    if (warmup == 0 || 2.0 * t1 > budget_s) {
+      secs_out[(*n_timed)++] = t1;
+    } else {
+      *n_warm = 1;
+    }
+    // more warm-ups only while the remaining timed epochs still fit
+    while (*n_warm > 0 && *n_warm < warmup && used + t1 * (1.0 + static_cast<double>(epochs)) <= budget_s) {
+      used += epoch();
+      ++*n_warm;
+    }
+    while (*n_timed < epochs && (*n_timed == 0 || used + t1 <= budget_s)) {
+      const double t = epoch();
+      used += t;
+      secs_out[(*n_timed)++] = t;
+    }
+  });
+}
+
 // ---- host I/O and the ratings generator (golden fixtures for the C++ host
 // API: tests/golden/make_io_golden.py).  Every call stores the exception text
 // for ref_last_message().

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <thread>
 #include <vector>
 
@@ -323,6 +324,47 @@ int sh_synth(int order, const uint32_t* dims, const double* zipf, uint64_t nnz, 
     });
   }
   return 0;
+}
+
+// train_test_split's id partition (sptensor.cpp:217-254; the device form is
+// sgdt_split_ids): Fisher-Yates of 0..nnz-1 with Rng(seed) -- j = i +
+// next_below(nnz - i) for i < nnz - 1 (rng.hpp:20-25) -- the first
+// llround(fraction nnz) positions are the test ids; both halves ascending.
+// The swaps run with the upcoming targets prefetched (the draws do not
+// depend on the array), and the halves are read off a membership flag
+// instead of sorted.  Returns ntest, or 0 for a degenerate split.
+uint64_t sh_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, uint32_t* test_ids, uint32_t* train_ids) {
+  if (!(test_fraction > 0.0 && test_fraction < 1.0)) return 0;
+  const uint64_t ntest = static_cast<uint64_t>(std::llround(test_fraction * static_cast<double>(nnz)));
+  if (ntest == 0 || ntest == nnz) return 0;
+  std::vector<uint32_t> ids(nnz);
+  for (uint64_t e = 0; e < nnz; ++e) ids[e] = static_cast<uint32_t>(e);
+  std::mt19937_64 eng(seed);
+  auto next_below = [&](uint64_t bound) {
+    const uint64_t threshold = (0 - bound) % bound;
+    for (;;) {
+      const uint64_t r = eng();
+      if (r >= threshold) return r % bound;
+    }
+  };
+  constexpr uint64_t kBatch = 1 << 16, kAhead = 24;
+  std::vector<uint64_t> js(kBatch);
+  for (uint64_t i0 = 0; i0 + 1 < nnz; i0 += kBatch) {
+    const uint64_t i1 = std::min(nnz - 1, i0 + kBatch);
+    for (uint64_t i = i0; i < i1; ++i) js[i - i0] = i + next_below(nnz - i);
+    for (uint64_t i = i0; i < i1; ++i) {
+      if (i + kAhead < i1) __builtin_prefetch(&ids[js[i + kAhead - i0]], 1);
+      std::swap(ids[i], ids[js[i - i0]]);
+    }
+  }
+  std::vector<uint8_t> in_test(nnz, 0);
+  for (uint64_t i = 0; i < ntest; ++i) in_test[ids[i]] = 1;
+  uint64_t a = 0, b = 0;
+  for (uint64_t e = 0; e < nnz; ++e) {
+    if (in_test[e]) test_ids[a++] = static_cast<uint32_t>(e);
+    else train_ids[b++] = static_cast<uint32_t>(e);
+  }
+  return ntest;
 }
 
 }  // extern "C"

@@ -176,3 +176,21 @@ def synth_host(dims, zipf, nnz: int, J: int, R: int, ratings: bool, noise: float
     if rc != 0:
         raise ValueError(f"sh_synth failed with code {rc}")
     return coords, values
+
+
+def split_ids_host(nnz: int, test_fraction: float, seed: int):
+    """(test_ids, train_ids) of train_test_split, by synth_host.cpp's
+    sh_split_ids (the reference's Fisher-Yates with Rng(seed), both halves
+    ascending)."""
+    import ctypes as C
+    L = _host_lib()
+    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+    L.sh_split_ids.argtypes = [C.c_uint64, C.c_double, C.c_uint64, u32p, u32p]
+    L.sh_split_ids.restype = C.c_uint64
+    ntest = int(round(test_fraction * nnz))
+    te = np.empty(max(ntest, 1), np.uint32)
+    tr = np.empty(max(nnz - ntest, 1), np.uint32)
+    got = L.sh_split_ids(nnz, test_fraction, seed, te, tr)
+    if got == 0:
+        raise ValueError("degenerate split")
+    return te[:got], tr[:nnz - got]

@@ -209,6 +209,7 @@ struct Session {
   uint64_t xfer_cap = 0;
 
   cudaEvent_t ev[4 + kMaxOrder] = {};
+  std::vector<cudaEvent_t> tev;  // per-epoch phase events of sgdt_run_epochs (timing means)
   sgdt_timing timing{};
   bool timing_valid = false;
   uint64_t launches = 0;  // kernels launched by this session

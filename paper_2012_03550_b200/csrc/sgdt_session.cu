@@ -613,6 +613,7 @@ void free_session(sgdt_session* s) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {s->ev_start, s->ev_core, s->ev_samp})
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->tev) cudaEventDestroy(e);
   if (s->side) cudaStreamDestroy(s->side);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -771,13 +772,15 @@ int ensure_subset(Session& s, int n, double fraction) {
   return SGDT_OK;
 }
 
-int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes) {
+// mode_ev (nullable): events recorded before each mode's launches.
+int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes, cudaEvent_t* mode_ev = nullptr) {
   if (h.lr == 0.0) return SGDT_OK;
   const bool subset = h.row_fraction < 1.0;
   if (subset && s.world > 1)
     return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not supported by the sharded (multi-GPU) factor phase");
   for (int n = 0; n < s.order; ++n) {
     if (time_modes) SGDT_CUDA(cudaEventRecord(s.ev[4 + n], s.stream));
+    if (mode_ev) SGDT_CUDA(cudaEventRecord(mode_ev[n], s.stream));
     if (subset) {
       // the draws of mode n follow mode n-1's update in the RNG stream
       // (factor_optimizer.cpp:384-424); they do not depend on the model.
@@ -808,6 +811,17 @@ int settle_ahead(Session& s, bool discard, const char* who) {
     return SGDT_OK;
   }
   return fail(SGDT_ERR_CONFIG, std::string(who) + ": a sgdt_sample_ahead draw is pending; run sgdt_core_epoch_async first");
+}
+
+constexpr uint64_t kTimedEpochs = 1024;
+
+int ensure_timing_events(Session& s, uint64_t n) {
+  while (s.tev.size() < n) {
+    cudaEvent_t e = nullptr;
+    SGDT_CUDA(cudaEventCreate(&e));
+    s.tev.push_back(e);
+  }
+  return SGDT_OK;
 }
 
 int sync_and_flag(Session& s) {
@@ -1307,10 +1321,17 @@ int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
       SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
     }
   }
+  // per-epoch phase events (the last kTimedEpochs epochs): {core start, core
+  // end, mode starts[N], factor end}; sgdt_last_timing reports their means
+  const int stride = s->order + 3;
+  const uint64_t timed = std::min<uint64_t>(epochs, kTimedEpochs);
+  TRY(ensure_timing_events(*s, timed * stride));
   for (uint64_t e = 0; e < epochs; ++e) {
     const bool last = e + 1 == epochs;
+    cudaEvent_t* E = e + timed >= epochs ? &s->tev[(e + timed - epochs) * stride] : nullptr;
     if (ahead) SGDT_CUDA(cudaStreamWaitEvent(s->stream, s->ev_samp, 0));
     if (last) SGDT_CUDA(cudaEventRecord(s->ev[0], s->stream));
+    if (E) SGDT_CUDA(cudaEventRecord(E[0], s->stream));
     TRY(enqueue_core(*s, *ch, m, ahead ? buf[e & 1] : nullptr));
     if (ahead && !last) {
       SGDT_CUDA(cudaEventRecord(s->ev_core, s->stream));
@@ -1319,8 +1340,10 @@ int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
       SGDT_CUDA(cudaEventRecord(s->ev_samp, s->side));
     }
     if (last) SGDT_CUDA(cudaEventRecord(s->ev[1], s->stream));
-    TRY(enqueue_factor(*s, *fh, last));
+    if (E) SGDT_CUDA(cudaEventRecord(E[1], s->stream));
+    TRY(enqueue_factor(*s, *fh, last, E ? E + 2 : nullptr));
     if (last) SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
+    if (E) SGDT_CUDA(cudaEventRecord(E[2 + s->order], s->stream));
   }
   if (out) {
     // copy-out on the side stream: B^(k) is final after the last core phase,
@@ -1349,12 +1372,21 @@ int run_epochs_impl(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_facto
     if (rc != SGDT_OK) return rc;
   }
   sgdt_timing t{};
-  SGDT_CUDA(cudaEventElapsedTime(&t.core_ms, s->ev[0], s->ev[1]));
-  SGDT_CUDA(cudaEventElapsedTime(&t.factor_ms, s->ev[1], s->ev[2]));
-  if (fh->lr > 0.0)
-    for (int n = 0; n < s->order; ++n)
-      SGDT_CUDA(cudaEventElapsedTime(&t.factor_mode_ms[n], s->ev[4 + n],
-                                     n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2]));
+  for (uint64_t e = 0; e < timed; ++e) {
+    cudaEvent_t* E = &s->tev[e * stride];
+    float core = 0.f, fac = 0.f;
+    SGDT_CUDA(cudaEventElapsedTime(&core, E[0], E[1]));
+    SGDT_CUDA(cudaEventElapsedTime(&fac, E[1], E[2 + s->order]));
+    t.core_ms += core / timed;
+    t.factor_ms += fac / timed;
+    if (fh->lr > 0.0)
+      for (int n = 0; n < s->order; ++n) {
+        float x = 0.f;
+        SGDT_CUDA(cudaEventElapsedTime(&x, E[2 + n], E[3 + n]));
+        t.factor_mode_ms[n] += x / timed;
+      }
+  }
+  t.epochs = static_cast<uint32_t>(timed);
   s->timing = t;
   s->timing_valid = true;
   return SGDT_OK;

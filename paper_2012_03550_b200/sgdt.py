@@ -75,7 +75,7 @@ class _FactorStats(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [("sample_ms", C.c_float), ("core_ms", C.c_float), ("factor_ms", C.c_float),
-                ("factor_mode_ms", C.c_float * MAX_ORDER)]
+                ("factor_mode_ms", C.c_float * MAX_ORDER), ("epochs", C.c_uint32)]
 
 
 _lib = None

@@ -25,7 +25,6 @@ from __future__ import annotations
 import dataclasses
 
 import numpy as np
-import torch
 
 
 @dataclasses.dataclass
@@ -70,6 +69,8 @@ def generate(spec: SynthSpec, device="cuda", with_perms: bool = False):
     device (csrc/sgdt_synth.cu); the 90/10 split is the reference's
     train_test_split (sptensor.cpp:217-254: Fisher-Yates with Rng(seed + 7),
     both halves in entry order), also on the device (sgdt_split_ids)."""
+    import torch
+
     from . import sgdt
     dev = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
     index = -1 if dev.type != "cuda" else (dev.index if dev.index is not None else torch.cuda.current_device())

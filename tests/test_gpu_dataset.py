@@ -21,13 +21,7 @@ def sg():
 def first_duplicate(coords, dims):
     """The reference's answer: smallest entry id whose coordinates occur at a
     smaller id (the hash-set insert order of sptensor.cpp:90-100)."""
-    key = np.zeros(len(coords), dtype=object) if np.prod([float(d) for d in dims]) >= 2.0 ** 63 else \
-        np.zeros(len(coords), np.int64)
-    stride = 1
-    for k, d in enumerate(dims):
-        key = key + (coords[:, k].astype(np.int64) - 1) * stride
-        stride *= int(d)
-    _, first = np.unique(key, return_index=True)
+    _, first = np.unique(coords, axis=0, return_index=True)
     mask = np.ones(len(coords), bool)
     mask[first] = False
     dup = np.flatnonzero(mask)

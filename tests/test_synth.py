@@ -102,3 +102,14 @@ def test_host_generator_matches_device_at_scale():
     hc, hv = S.synth_host(*args)
     assert np.array_equal(c, hc)
     assert np.mean(v != hv) < 1e-4  # ratings: a rounding tie may flip in a rare entry
+
+
+@pytest.mark.parametrize("nnz,frac,seed", [(10, 0.1, 1), (1000, 0.25, 7), (200_003, 0.1, 8)])
+def test_host_split_matches_oracle(nnz, frac, seed):
+    from oracle import oracle_py as O
+    import ctypes as C
+    ids = np.empty(nnz, np.uint32)
+    nt = C.c_size_t()
+    assert O.lib().or_train_test_split_ids(nnz, frac, seed, ids, C.byref(nt)) == 0
+    te, tr = S.split_ids_host(nnz, frac, seed)
+    assert np.array_equal(te, ids[:nt.value]) and np.array_equal(tr, ids[nt.value:])
