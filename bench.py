@@ -321,6 +321,46 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+def cpp_dropin_e2e(cfg, spec, trc, trv, m, warmup, steps):
+    """End to end through the C++ drop-in (libsptucker_b200.so): a
+    sptucker::CooTensor built from the host arrays, then the reference's
+    timed_epochs loop (eval.cpp:201-223) -- update_core_epoch +
+    update_factor_epoch on a host fp64 TuckerModel, host wall clock per epoch,
+    median -- through paper_2012_03550_b200/cpp/tools/bench_shim.cpp."""
+    import ctypes as C
+    so = os.path.join(ROOT, "paper_2012_03550_b200", "lib", "libsptucker_bench.so")
+    L = C.CDLL(so)
+    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+    f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    L.sptb_timed_epochs.argtypes = [C.c_int, u32p, C.c_uint64, u32p, f64p, u32p, C.c_uint32, C.c_double, C.c_double,
+                                    C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                    C.c_double, f64p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                    C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+    order = len(spec.dims)
+    J = R = spec.teacher_j
+    mean, sd = init_stats(cfg, spec)
+    secs = np.zeros(max(steps, 1))
+    h2d, d2h, build = C.c_uint64(), C.c_uint64(), C.c_double()
+    err = C.create_string_buffer(512)
+    rc = L.sptb_timed_epochs(order, np.ascontiguousarray(spec.dims, np.uint32), len(trv),
+                             np.ascontiguousarray(trc, np.uint32).reshape(-1), np.ascontiguousarray(trv),
+                             np.full(order, J, np.uint32), R, HYPER["lr_a"], HYPER["lr_b"], HYPER["reg_a"], m,
+                             warmup, max(steps, 1), HYPER["seed"], mean, sd, secs, C.byref(h2d), C.byref(d2h),
+                             C.byref(build), err, 512)
+    if rc != 0:
+        raise RuntimeError(err.value.decode(errors="replace"))
+    units = units_per_epoch(order, m, len(trv))
+    med = float(np.median(secs))
+    n = max(steps, 1)
+    return {"value": units / med, "unit": "updates/s", "ms_per_step": med * 1e3,
+            "h2d_bytes_per_step": int(h2d.value) // n, "d2h_bytes_per_step": int(d2h.value) // n,
+            "path": "C++ drop-in (libsptucker_b200.so): sptucker::CooTensor + the reference's timed_epochs loop "
+                    "(update_core_epoch + update_factor_epoch on a host fp64 TuckerModel per epoch; model and sample "
+                    "pool stay device-resident between calls, B / A / pool deltas copied back every epoch), "
+                    "host wall clock, median",
+            "epoch_ms": [float(x) * 1e3 for x in secs], "tensor_build_s": build.value}
+
+
 def factor_traffic(cfg, mode_ms, peak):
     """ncu DRAM / L2 bytes per factor-mode launch group of THIS build
     (profiles/factor_traffic.json, written by scripts/ncu_factor_traffic.py,
@@ -511,7 +551,7 @@ def run_ours(args, rank, world, local_rank):
     rmse = s.eval(1)[0]
 
     # end to end through the C-ABI with host buffers: H2D model, epoch, D2H model
-    e2e = None
+    e2e = e2e_cabi = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
         hA, hB = [pin(a) for a in A], [pin(b) for b in B]
@@ -535,9 +575,15 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.steps
-        e2e = {"value": units / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "sgdt_run_epochs_host(1): fp64 pinned host model in -> epoch -> fp64 pinned host model out"}
+        e2e_cabi = {"value": units / (e_ms * 1e-3), "unit": "updates/s", "ms_per_step": e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "sgdt_run_epochs_host(1): fp64 pinned host model in -> epoch -> fp64 pinned host model out"}
+    s.close()  # the device memory goes to the drop-in's own session
+    if not args.no_e2e:
+        try:
+            e2e = cpp_dropin_e2e(cfg, spec, trc, trv, m, args.warmup, args.steps)
+        except Exception as exc:  # reported; the C-ABI figure stands in
+            e2e = dict(e2e_cabi or {}, error=f"C++ drop-in leg failed: {type(exc).__name__}: {exc}")
 
     cpu = None
     if rank == 0 and cfg in REF_UNAVAILABLE and not args.no_cpu_baseline:
@@ -574,6 +620,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "e2e_cabi": e2e_cabi,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary: plain pointers, sizes and POD structs, no
  * exceptions and no torch types.  The C++ host API that mirrors the reference
- * (paper_2012_03550_b200/cpp/include/sptucker/*.hpp, namespace sptucker) sits on
+ * (paper_2012_03550_b200/cpp/include/sptucker/ headers, namespace sptucker) sits on
  * top of it, exactly as the reference's per-epoch calls sit on top of its CPU
  * loops.  Each entry point names the reference interface it replaces
  * (paths relative to /root/reference/proj).
@@ -100,6 +100,20 @@ typedef struct {
 
 const char* sgdt_last_error(void);
 const char* sgdt_version(void);
+/* Number of CUDA devices visible (0 without a GPU or driver). */
+int sgdt_device_count(void);
+
+/* The CooTensor constructor's work on the device (sptensor.cpp:80-118): the
+ * coordinate range and duplicate checks -- DataError "entry <e>: coordinate
+ * out of range" / "entry <e>: duplicate coordinate" at the first failing
+ * entry, range first, as the reference's entry-by-entry loop reports it --
+ * and, for each mode n with a non-NULL perm_out[n] / offsets_out[n] (host
+ * buffers of nnz / I_n + 1 entries), CooTensor::mode_perm(n) (entry ids
+ * bucketed by i_n, ascending inside a bucket; a stable radix sort) and
+ * mode_offsets(n) (offsets[0] = 0, offsets[i] = end of bucket i).
+ * perm_out / offsets_out may be NULL (checks only). */
+int sgdt_tensor_layout(const sgdt_tensor_desc* t, int device, uint32_t* const* perm_out,
+                       uint64_t* const* offsets_out);
 
 /* Upload a training tensor (and optional test tensor, may be NULL) and size
  * the device model for ranks J (N entries) and R.  Builds the entry-order
@@ -116,7 +130,8 @@ void sgdt_session_destroy(sgdt_session* s);
 void* sgdt_session_stream(sgdt_session* s);
 
 /* Model state in/out, fp64 host <-> fp32 device.  A[n] is I_n x J_n, B[n] is
- * J_n x R (TuckerModel::factor/kruskal, model.hpp:54-58). */
+ * J_n x R (TuckerModel::factor/kruskal, model.hpp:54-58).  sgdt_get_model
+ * skips A (or B) when that argument is NULL (a phase changed only the other). */
 int sgdt_set_model(sgdt_session* s, const double* const* A, const double* const* B);
 int sgdt_get_model(sgdt_session* s, double* const* A, double* const* B);
 
@@ -144,6 +159,19 @@ int sgdt_last_batch(sgdt_session* s, uint32_t* out, uint64_t* len);
 int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* st);
 /* update_factor_epoch (factor_optimizer.cpp:101-273). */
 int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_stats* st);
+/* update_factor_epoch on a host Model& (the drop-in's per-epoch call): the
+ * factor passes, with A^(n) copied out to A_out[n] (fp64 host, pageable or
+ * pinned) as soon as mode n is final -- the copy of mode n overlaps the
+ * passes of the later modes.  B is not touched. */
+int sgdt_factor_epoch_host(sgdt_session* s, const sgdt_factor_hyper* h, double* const* A_out,
+                           sgdt_factor_stats* st);
+/* The persistent pool's change from the last sgdt_core_epoch / sgdt_sample_batch
+ * call (exactly one sampler run of m draws): pos[i] = j_i (the draw targets,
+ * sample_batch's partial Fisher-Yates) and val[i] = pool[j_i] afterwards, for
+ * i < m; with positions < m holding the batch, applying them to the previous
+ * host pool gives the new one.  *n = m.  SGDT_ERR_CONFIG when the last call
+ * made no or several sampler runs (resample_per_mode): use sgdt_get_pool. */
+int sgdt_pool_delta(sgdt_session* s, uint32_t* pos, uint32_t* val, uint64_t* n);
 /* `epochs` x (core phase; factor phase) enqueued back to back, one host
  * synchronisation at the end (the timed part of train(), trainer.cpp:94-107).
  * A divergence anywhere returns SGDT_ERR_NUMERIC (trainer.cpp:101-103). */

@@ -20,6 +20,7 @@ ROOT = _build.ROOT
 CPP = os.path.join(PKG, "cpp")
 LIB = os.path.join(_build.LIBDIR, "libsptucker_b200.so")
 TEST_BIN = os.path.join(_build.LIBDIR, "test_sptucker")
+SHIM = os.path.join(_build.LIBDIR, "libsptucker_bench.so")
 CXX = os.environ.get("CXX", "g++")
 FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(CPP, "include")]
 
@@ -39,6 +40,14 @@ def build(force: bool = False, test: bool = True) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"C++ host build failed:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
         os.replace(LIB + ".tmp", LIB)
+    shim_src = os.path.join(CPP, "tools", "bench_shim.cpp")
+    if force or _stale(SHIM, [shim_src, LIB] + deps):
+        cmd = [CXX, *FLAGS, "-shared", "-o", SHIM + ".tmp", shim_src, "-L", _build.LIBDIR, "-lsptucker_b200",
+               "-lsgdt", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"bench shim build failed:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
+        os.replace(SHIM + ".tmp", SHIM)
     if test:
         build_test(force)
     return LIB

@@ -2,6 +2,8 @@
 // the error-code mapping (include/sgdt.h codes -> sptucker exceptions).
 #include "device.hpp"
 
+#include <algorithm>
+#include <numeric>
 #include <string>
 
 namespace sptucker::detail {
@@ -30,6 +32,13 @@ sgdt_tensor_desc describe(const CooTensor& t, const std::vector<std::uint32_t>& 
   d.values = t.values().data();
   d.mode_perm = perms.data();
   return d;
+}
+
+std::uint64_t model_bytes(const TuckerModel& m, bool factors, bool kruskal) {
+  std::uint64_t b = 0;
+  for (std::size_t n = 0; n < m.order(); ++n)
+    b += (factors ? m.factor(n).size() : 0) + (kruskal ? m.kruskal(n).size() : 0);
+  return b * sizeof(double);
 }
 }  // namespace
 
@@ -63,24 +72,86 @@ void Session::put_model(const TuckerModel& m) {
 }
 
 void Session::take_model(TuckerModel& m, bool factors, bool kruskal) {
-  std::vector<std::vector<double>> scratch;
   std::vector<double*> a(m.order()), b(m.order());
   for (std::size_t n = 0; n < m.order(); ++n) {
-    if (factors) {
-      a[n] = m.factor(n).data().data();
-    } else {
-      scratch.emplace_back(m.factor(n).size());
-      a[n] = scratch.back().data();
-    }
-    if (kruskal) {
-      b[n] = m.kruskal(n).data().data();
-    } else {
-      scratch.emplace_back(m.kruskal(n).size());
-      b[n] = scratch.back().data();
-    }
+    if (factors) a[n] = m.factor(n).data().data();
+    if (kruskal) b[n] = m.kruskal(n).data().data();
   }
-  check(sgdt_get_model(h_, a.data(), b.data()), "download model");
+  check(sgdt_get_model(h_, factors ? a.data() : nullptr, kruskal ? b.data() : nullptr), "download model");
+  d2h_bytes += model_bytes(m, factors, kruskal);
   if (kruskal) m.refresh_core_cache();
+  mark_synced(m);
+}
+
+void Session::sync_model(const TuckerModel& m) {
+  if (synced_model_ == &m && synced_gen_ == m.generation()) return;
+  put_model(m);
+  h2d_bytes += model_bytes(m, true, true);
+  mark_synced(m);
+}
+
+void Session::mark_synced(const TuckerModel& m) {
+  synced_model_ = &m;
+  synced_gen_ = m.generation();
+}
+
+sgdt_factor_stats Session::factor_epoch_into(TuckerModel& m, const sgdt_factor_hyper& h) {
+  std::vector<double*> a(m.order());
+  for (std::size_t n = 0; n < m.order(); ++n) a[n] = m.factor(n).data().data();
+  sgdt_factor_stats st{};
+  const int rc = sgdt_factor_epoch_host(h_, &h, a.data(), &st);
+  if (rc == SGDT_OK || rc == SGDT_ERR_NUMERIC) {
+    if (h.lr > 0.0) d2h_bytes += model_bytes(m, true, false);
+    mark_synced(m);  // the host A is what the device holds, even on divergence
+  }
+  check(rc, "update_factor_epoch");
+  return st;
+}
+
+std::uint64_t Session::fingerprint(const std::vector<std::uint32_t>& pool) {
+  // 4096 strided words and the last one, mixed (splitmix64 finaliser)
+  std::uint64_t h = pool.size() * 0x9E3779B97F4A7C15ull;
+  const std::size_t n = pool.size(), step = n / 4096 + 1;
+  auto mix = [&](std::uint64_t v) {
+    h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+  };
+  for (std::size_t i = 0; i < n; i += step) mix((static_cast<std::uint64_t>(i) << 32) | pool[i]);
+  if (n) mix(pool[n - 1]);
+  return h;
+}
+
+void Session::sync_pool(const std::vector<std::uint32_t>& pool) {
+  if (pool.data() == pool_data_ && pool.size() == pool_size_ && fingerprint(pool) == pool_fp_) return;
+  check(sgdt_set_pool(h_, pool.data()), "update_core_epoch");
+  h2d_bytes += pool.size() * sizeof(std::uint32_t);
+  pool_data_ = pool.data();
+  pool_size_ = pool.size();
+  pool_fp_ = fingerprint(pool);
+}
+
+void Session::pool_reset(const std::vector<std::uint32_t>& iota_pool) {
+  check(sgdt_reset_pool(h_), "update_core_epoch");
+  pool_data_ = iota_pool.data();
+  pool_size_ = iota_pool.size();
+  pool_fp_ = fingerprint(iota_pool);
+}
+
+void Session::pool_after_epoch(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch) {
+  std::vector<std::uint32_t> pos(batch.size()), val(batch.size());
+  std::uint64_t n = 0;
+  if (sgdt_pool_delta(h_, pos.data(), val.data(), &n) == SGDT_OK) {
+    for (std::uint64_t i = 0; i < n; ++i) pool[pos[i]] = val[i];
+    std::copy(batch.begin(), batch.end(), pool.begin());
+    d2h_bytes += 2 * n * sizeof(std::uint32_t);
+  } else {  // several draws (resample_per_mode): the whole pool
+    check(sgdt_get_pool(h_, pool.data()), "update_core_epoch");
+    d2h_bytes += pool.size() * sizeof(std::uint32_t);
+  }
+  pool_data_ = pool.data();
+  pool_size_ = pool.size();
+  pool_fp_ = fingerprint(pool);
 }
 
 void Session::put_rng(const Rng& r) { check(sgdt_set_rng(h_, r.state_words().data(), r.state_pos()), "rng"); }

@@ -29,8 +29,33 @@ class Session {
   void put_rng(const Rng& r);
   void take_rng(Rng& r);
 
+  // Device residency across the per-epoch calls: the session remembers which
+  // model (object and generation) its device copy equals and uploads only
+  // when that changed; after a phase it downloads only what the phase wrote
+  // (B after the core phase, A -- overlapped with the later modes -- after
+  // the factor phase) and records the new generation.
+  void sync_model(const TuckerModel& m);
+  void mark_synced(const TuckerModel& m);
+  // The factor epoch with the A^(n) copy-out overlapped (sgdt_factor_epoch_host).
+  sgdt_factor_stats factor_epoch_into(TuckerModel& m, const sgdt_factor_hyper& h);
+  // The persistent sample pool: uploaded only when the workspace's pool is
+  // not the one this session last wrote (buffer, size or fingerprint
+  // differ); after a core epoch only the touched positions come back.
+  void sync_pool(const std::vector<std::uint32_t>& pool);
+  void pool_reset(const std::vector<std::uint32_t>& iota_pool);  // the host pool was just set to iota
+  void pool_after_epoch(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch);
+
+  std::uint64_t h2d_bytes = 0, d2h_bytes = 0;  // model / pool / batch traffic of the per-epoch calls
+
  private:
+  static std::uint64_t fingerprint(const std::vector<std::uint32_t>& pool);
+
   sgdt_session* h_ = nullptr;
+  const TuckerModel* synced_model_ = nullptr;
+  std::uint64_t synced_gen_ = 0;
+  const std::uint32_t* pool_data_ = nullptr;
+  std::size_t pool_size_ = 0;
+  std::uint64_t pool_fp_ = 0;
   const CooTensor* test_ = nullptr;
   std::size_t test_nnz_ = 0;
   std::vector<std::uint32_t> dims_, J_;

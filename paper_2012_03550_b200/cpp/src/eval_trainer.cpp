@@ -1,12 +1,15 @@
 // eval_trainer.cpp -- rmse_mae and train() on the device; small host utilities.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <limits>
 #include <thread>
 
 #include "device.hpp"
+#include "sptucker/core_optimizer.hpp"
 #include "sptucker/eval.hpp"
+#include "sptucker/factor_optimizer.hpp"
 #include "sptucker/trainer.hpp"
 
 namespace sptucker {
@@ -17,7 +20,7 @@ std::pair<double, double> rmse_mae(const TuckerModel& model, const CooTensor& en
     if (entries.shape().dim(n) > model.shape().dim(n))
       throw DomainError("rmse_mae: data exceeds the model's shape in mode " + std::to_string(n + 1));
   detail::Session& s = detail::session_for(entries, nullptr, model.shape(), model.ranks());
-  s.put_model(model);
+  s.sync_model(model);
   double rmse = 0.0, mae = 0.0;
   detail::check(sgdt_eval(s.get(), 0, &rmse, &mae), "rmse_mae");
   return {rmse, mae};
@@ -63,6 +66,78 @@ LinearFit fit_linear(const std::vector<double>& x, const std::vector<double>& y)
   f.intercept = my - f.slope * mx;
   f.r2 = syy == 0.0 ? 1.0 : sxy * sxy / (sxx * syy);
   return f;
+}
+
+std::vector<double> timed_epoch_seconds(const CooTensor& train, const Ranks& ranks, const BenchOptions& opts,
+                                        double init_mean, double init_stddev, std::uint64_t* workspace_bytes) {
+  TuckerModel model = TuckerModel::init_gaussian(train.shape(), ranks, init_mean, init_stddev, opts.seed);
+  Rng rng(opts.seed + 1);
+  const CoreHyper core{opts.lr_b, opts.reg, opts.batch_m, false, false};
+  const FactorHyper factor{opts.lr_a, opts.reg, 1.0};
+  WorkerPool pool(std::max<std::size_t>(1, opts.threads));
+  const SchedContext sched{opts.threads <= 1 ? Strategy::Serial : opts.strategy, BalancePolicy::Dynamic,
+                           opts.threads <= 1 ? nullptr : &pool};
+  CoreBatchWorkspace core_ws;
+  std::vector<RowBatchWorkspace> row_ws(sched.workers());
+  std::vector<double> seconds;
+  for (std::size_t ep = 0; ep < opts.warmup + opts.epochs; ++ep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    update_core_epoch(model, train, core, sched, rng, core_ws);
+    update_factor_epoch(model, train, factor, sched, rng, row_ws);
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (ep >= opts.warmup) seconds.push_back(s);
+  }
+  if (workspace_bytes) {
+    *workspace_bytes = core_ws.bytes();
+    for (const auto& ws : row_ws) *workspace_bytes += ws.bytes();
+  }
+  return seconds;
+}
+
+namespace {
+double median_of(std::vector<double> v) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const std::size_t k = v.size();
+  return k % 2 ? v[k / 2] : 0.5 * (v[k / 2 - 1] + v[k / 2]);
+}
+}  // namespace
+
+RankScalingResult bench_rank_scaling(const CooTensor& train, const std::vector<Ranks>& grid,
+                                     const std::vector<std::uint32_t>& x_values, const BenchOptions& opts) {
+  if (grid.size() != x_values.size()) throw DomainError("bench_rank_scaling: grid and x values differ in length");
+  RankScalingResult out;
+  std::vector<double> xs, times, bytes;
+  for (std::size_t i = 0; i < grid.size(); ++i) {
+    std::uint64_t ws_bytes = 0;
+    const double secs = median_of(timed_epoch_seconds(train, grid[i], opts, 0.5, 0.1, &ws_bytes));
+    out.rows.push_back({x_values[i], secs, ws_bytes});
+    xs.push_back(static_cast<double>(x_values[i]));
+    times.push_back(secs);
+    bytes.push_back(static_cast<double>(ws_bytes));
+  }
+  out.time_fit = fit_linear(xs, times);
+  out.bytes_fit = fit_linear(xs, bytes);
+  return out;
+}
+
+std::vector<SpeedupRow> bench_speedup(const CooTensor& train, const Ranks& ranks,
+                                      const std::vector<std::size_t>& thread_grid, const BenchOptions& opts) {
+  std::vector<SpeedupRow> out;
+  double t1 = 0.0;
+  for (const std::size_t threads : thread_grid) {
+    BenchOptions o = opts;
+    o.threads = threads;
+    const double secs = median_of(timed_epoch_seconds(train, ranks, o, 0.5, 0.1));
+    if (threads == 1 && t1 == 0.0) t1 = secs;
+    SpeedupRow row;
+    row.threads = threads;
+    row.seconds_per_epoch = secs;
+    row.speedup = (threads == 1 && secs == t1) ? 1.0 : (t1 > 0.0 ? t1 / secs : 0.0);
+    row.efficiency = row.speedup / static_cast<double>(threads);
+    out.push_back(row);
+  }
+  return out;
 }
 
 void HyperParams::validate() const {
@@ -133,7 +208,7 @@ TrainResult train(TuckerModel& model, const CooTensor& train_set, const CooTenso
   }
 
   detail::Session& s = detail::session_for(train_set, test_set, model.shape(), model.ranks(), hyper.device);
-  s.put_model(model);
+  s.sync_model(model);
   Rng rng(hyper.seed + 1);  // batch stream, trainer.cpp:72
   s.put_rng(rng);
   detail::check(sgdt_reset_pool(s.get()), "train");  // fresh workspace: pool restarts from iota

@@ -4,10 +4,16 @@
 #include "sptucker/model.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <limits>
 #include <string>
 
 namespace sptucker {
+
+std::uint64_t ModelGeneration::next() {
+  static std::atomic<std::uint64_t> counter{0};
+  return ++counter;
+}
 
 void Ranks::validate(std::size_t order) const {
   if (J.size() != order) throw DomainError("ranks: J arity does not match tensor order");
@@ -85,7 +91,10 @@ TuckerModel TuckerModel::init_gaussian(const Shape& shape, const Ranks& ranks, d
   return m;
 }
 
-void TuckerModel::refresh_core_cache() { core_fresh_ = false; }
+void TuckerModel::refresh_core_cache() {
+  core_fresh_ = false;
+  gen_.bump();  // callers refresh after editing B through a held reference
+}
 
 void TuckerModel::build_core_cache() const {
   if (core_fresh_) return;

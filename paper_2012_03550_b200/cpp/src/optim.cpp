@@ -170,27 +170,32 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
   const std::size_t m = hyper.batch_m == 0 ? nnz : hyper.batch_m;
   if (m > nnz) throw DomainError("core batch size exceeds training nnz");
 
+  // device-resident across calls: the model and the pool go up only when
+  // the host copies changed since this session last synchronised them
   detail::Session& s = detail::session_for(train, nullptr, model.shape(), model.ranks());
-  s.put_model(model);
+  s.sync_model(model);
   s.put_rng(rng);
   if (hyper.batch_m != 0) {
-    if (ws.sample_pool.size() != nnz) {
+    if (ws.sample_pool.size() != nnz) {  // sample_batch: a pool of the wrong size restarts from iota
       ws.grow(ws.sample_pool, nnz);
       std::iota(ws.sample_pool.begin(), ws.sample_pool.end(), 0u);
+      s.pool_reset(ws.sample_pool);
+    } else {
+      s.sync_pool(ws.sample_pool);
     }
-    detail::check(sgdt_set_pool(s.get(), ws.sample_pool.data()), "update_core_epoch");
   }
   const sgdt_core_hyper h{hyper.lr, hyper.reg, hyper.batch_m, hyper.resample_per_mode ? 1 : 0,
                           hyper.incremental_residual ? 1 : 0};
   sgdt_core_stats st{};
   detail::check(sgdt_core_epoch(s.get(), &h, &st), "update_core_epoch");
-  s.take_model(model, /*factors=*/false, /*kruskal=*/true);
+  s.take_model(model, /*factors=*/false, /*kruskal=*/true);  // the core phase wrote B only
   s.take_rng(rng);
   ws.grow(ws.batch, m);
   if (hyper.batch_m != 0) {
-    detail::check(sgdt_get_pool(s.get(), ws.sample_pool.data()), "update_core_epoch");
     std::uint64_t len = 0;
     detail::check(sgdt_last_batch(s.get(), ws.batch.data(), &len), "update_core_epoch");
+    s.d2h_bytes += m * sizeof(std::uint32_t);
+    s.pool_after_epoch(ws.sample_pool, ws.batch);
   } else {
     std::iota(ws.batch.begin(), ws.batch.end(), 0u);
   }
@@ -213,12 +218,10 @@ FactorEpochStats update_factor_epoch(TuckerModel& model, const CooTensor& train,
     for (std::vector<double>* v : {&w.e, &w.fact1, &w.fact2, &w.grad}) w.grow(*v, jmax);
 
   detail::Session& s = detail::session_for(train, nullptr, model.shape(), model.ranks());
-  s.put_model(model);
+  s.sync_model(model);
   s.put_rng(rng);
   const sgdt_factor_hyper h{hyper.lr, hyper.reg, hyper.row_fraction};
-  sgdt_factor_stats st{};
-  detail::check(sgdt_factor_epoch(s.get(), &h, &st), "update_factor_epoch");
-  s.take_model(model, /*factors=*/true, /*kruskal=*/false);
+  const sgdt_factor_stats st = s.factor_epoch_into(model, h);  // A^(n) copied out per mode, overlapped
   s.take_rng(rng);
 
   FactorEpochStats out;

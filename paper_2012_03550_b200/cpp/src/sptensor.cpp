@@ -112,8 +112,33 @@ CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector
   if (nnz == 0) throw DataError("tensor has no entries");
   if (coords_.size() != nnz * order) throw DataError("coords/values length mismatch");
   if (nnz > std::numeric_limits<std::uint32_t>::max()) throw DataError("entry count exceeds the 32-bit id space");
-  // The reference checks entry by entry, range before duplicate; the first
-  // failing entry decides the message.  Entries before the first out-of-range
+  mode_perm_.assign(order, std::vector<std::uint32_t>(nnz));
+  mode_offsets_.assign(order, {});
+  if (sgdt_device_count() > 0) {
+    // on the device (sgdt_tensor_layout): range + duplicate checks by a radix
+    // sort of packed coordinate keys, the N stable bucket sorts
+    std::vector<std::uint32_t*> perm(order);
+    std::vector<std::uint64_t*> off(order);
+    for (std::size_t n = 0; n < order; ++n) {
+      mode_offsets_[n].assign(static_cast<std::size_t>(shape_.dim(n)) + 1, 0);
+      perm[n] = mode_perm_[n].data();
+      off[n] = mode_offsets_[n].data();
+    }
+    const std::vector<std::uint32_t>& dims = shape_.dims();
+    sgdt_tensor_desc d{};
+    d.order = static_cast<int>(order);
+    d.dims = dims.data();
+    d.nnz = nnz;
+    d.coords = coords_.data();
+    d.values = values_.data();
+    const int rc = sgdt_tensor_layout(&d, -1, perm.data(), off.data());
+    if (rc == SGDT_ERR_DATA) throw DataError(sgdt_last_error());
+    detail::check(rc, "CooTensor");
+    return;
+  }
+  // Without a device (file tooling, the CPU test suite) the same layout is
+  // built on host threads.  The reference checks entry by entry, range
+  // before duplicate; the first failing entry decides the message.  Entries before the first out-of-range
   // one are all in range, so a duplicate found below it is exact.
   std::size_t bad_range = nnz;
   for (std::size_t e = 0; e < nnz && bad_range == nnz; ++e)
@@ -131,8 +156,6 @@ CooTensor::CooTensor(Shape shape, std::vector<std::uint32_t> coords, std::vector
   // Stable counting sort per mode: bucket i holds the entries with i_n = i in
   // ascending entry id (the order the device mode copies inherit); one host
   // thread per mode.
-  mode_perm_.assign(order, {});
-  mode_offsets_.assign(order, {});
   auto bucket_mode = [&](std::size_t n) {
     std::vector<std::uint64_t>& off = mode_offsets_[n];
     off.assign(static_cast<std::size_t>(shape_.dim(n)) + 1, 0);
@@ -202,17 +225,19 @@ void sample_batch(const CooTensor& t, std::size_t m, Rng& rng, std::vector<std::
                   std::vector<std::uint32_t>& out) {
   const std::size_t nnz = t.nnz();
   if (m < 1 || m > nnz) throw DomainError("sample_batch: batch size out of range");
+  detail::Session& s = sampler_session(t);
   if (pool.size() != nnz) {
     pool.resize(nnz);
     std::iota(pool.begin(), pool.end(), 0u);
+    s.pool_reset(pool);
+  } else {
+    s.sync_pool(pool);  // uploaded only if it is not the pool this session last wrote
   }
-  detail::Session& s = sampler_session(t);
-  detail::check(sgdt_set_pool(s.get(), pool.data()), "sample_batch");
   s.put_rng(rng);
   out.resize(m);
   detail::check(sgdt_sample_batch(s.get(), m, out.data()), "sample_batch");
   s.take_rng(rng);
-  detail::check(sgdt_get_pool(s.get(), pool.data()), "sample_batch");
+  s.pool_after_epoch(pool, out);  // the touched positions only
 }
 
 std::vector<std::uint32_t> sample_batch(const CooTensor& t, std::size_t m, Rng& rng) {

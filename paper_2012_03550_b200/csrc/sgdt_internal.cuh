@@ -178,6 +178,9 @@ struct Session {
   uint32_t* batch = nullptr;    // 2 x order x m: double-buffered Psi (one per mode when resampling)
   uint64_t batch_cap = 0;
   uint64_t last_batch_len = 0;
+  uint64_t sampler_runs = 0;  // launch_sampler calls (sgdt_pool_delta: exactly one since delta_base)
+  uint64_t delta_base = ~0ull;
+  uint64_t delta_m = 0;       // m of the last sampler run
   uint32_t* last_batch = nullptr;  // points into batch
   // sgdt_sample_ahead: the next core phase's Psi, drawn on the side stream
   bool ahead_valid = false;
@@ -209,6 +212,9 @@ struct Session {
   uint64_t xfer_cap = 0;
 
   cudaEvent_t ev[4 + kMaxOrder] = {};
+  cudaEvent_t ev_copy[kMaxOrder] = {};  // sgdt_factor_epoch_host: A^(n) landed in hx
+  double* hx = nullptr;                 // pinned fp64 staging of A (sgdt_factor_epoch_host)
+  uint64_t hx_cap = 0;
   std::vector<cudaEvent_t> tev;  // per-epoch phase events of sgdt_run_epochs (timing means)
   sgdt_timing timing{};
   bool timing_valid = false;

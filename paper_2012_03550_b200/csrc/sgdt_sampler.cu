@@ -586,6 +586,8 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st)
   s.launches += 4;
   s.last_batch = out_batch;
   s.last_batch_len = m;
+  ++s.sampler_runs;
+  s.delta_m = m;
   return SGDT_OK;
 }
 

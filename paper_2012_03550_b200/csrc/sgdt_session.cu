@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sgdt_internal.cuh"
@@ -94,6 +95,24 @@ unsigned grid_for(uint64_t n, int num_sms) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<unsigned>(g);
+}
+
+// memcpy on several host threads (pinned staging -> pageable caller memory).
+void parallel_copy(void* dst, const void* src, uint64_t bytes) {
+  const uint64_t kMin = 4ull << 20;
+  unsigned t = std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()));
+  if (bytes < kMin * 2 || t < 2) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  t = static_cast<unsigned>(std::min<uint64_t>(t, bytes / kMin));
+  std::vector<std::thread> th;
+  for (unsigned i = 1; i < t; ++i) {
+    const uint64_t b = bytes * i / t, e = bytes * (i + 1) / t;
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b); });
+  }
+  std::memcpy(dst, src, bytes / t);
+  for (auto& x : th) x.join();
 }
 
 // std::mt19937_64 seeding (the default engine state before set_rng).
@@ -278,7 +297,8 @@ __global__ void check_coords_kernel(const uint32_t* __restrict__ idx, uint64_t n
       if (idx[static_cast<uint64_t>(k) * nnz + e] >= dims.d[k]) atomicMin(first_bad, static_cast<unsigned long long>(e));
 }
 
-int check_coords(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, const char* what) {
+// The smallest entry id with a coordinate outside [1, I_k] (~0 if none).
+int first_bad_coord(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, uint64_t* out) {
   DimList dl{};
   for (int k = 0; k < d->order; ++k) dl.d[k] = d->dims[k];
   unsigned long long* bad = nullptr;
@@ -288,6 +308,7 @@ int check_coords(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, co
   if (cudaMemcpyAsync(bad, &h, sizeof h, cudaMemcpyHostToDevice, s.stream) != cudaSuccess) rc_ = SGDT_ERR_INTERNAL;
   if (rc_ == SGDT_OK) {
     check_coords_kernel<<<grid_for(rc.nnz, s.num_sms), 256, 0, s.stream>>>(rc.idx, rc.nnz, d->order, dl, bad);
+    ++s.launches;
     if (cudaGetLastError() != cudaSuccess ||
         cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, s.stream) != cudaSuccess ||
         cudaStreamSynchronize(s.stream) != cudaSuccess)
@@ -296,13 +317,31 @@ int check_coords(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, co
   cudaFree(bad);
   if (rc_ != SGDT_OK) {
     cudaGetLastError();
-    return fail(SGDT_ERR_INTERNAL, std::string(what) + ": coordinate check failed");
+    return fail(SGDT_ERR_INTERNAL, "coordinate check failed");
   }
-  if (h != ~0ull)
-    return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(h) + ": coordinate out of range");
+  *out = h;
   return SGDT_OK;
 }
 
+int first_duplicate(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, uint64_t* out);
+
+// The CooTensor constructor's checks (sptensor.cpp:80-100): entry by entry,
+// range before duplicate, the first failing entry decides the DataError.
+// Entries below the first out-of-range one are all in range, so a duplicate
+// found below it is the reference's answer.
+int check_entries(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, const std::string& prefix) {
+  uint64_t bad = ~0ull, dup = ~0ull;
+  TRY(first_bad_coord(s, rc, d, &bad));
+  TRY(first_duplicate(s, rc, d, &dup));
+  if (dup < bad) return fail(SGDT_ERR_DATA, prefix + "entry " + std::to_string(dup) + ": duplicate coordinate");
+  if (bad != ~0ull) return fail(SGDT_ERR_DATA, prefix + "entry " + std::to_string(bad) + ": coordinate out of range");
+  return SGDT_OK;
+}
+
+// (An out-of-range value overflows its field and can give two different
+// tuples one key; equal tuples always share a key, and a repeat that such a
+// key separates from its partner lies above an out-of-range entry, which
+// the reference reports first -- check_entries takes the smaller id.)
 // Duplicate detection (the CooTensor constructor's hash-set pass,
 // sptensor.cpp:90-100), as a sort: every entry's coordinates are packed into
 // a bit string of sum_k ceil(log2 I_k) bits (equal strings <=> equal
@@ -342,8 +381,10 @@ __global__ void dup_adjacent_kernel(const uint32_t* __restrict__ idx, uint64_t n
   }
 }
 
-int check_duplicates(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, const char* what) {
+int first_duplicate(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d, uint64_t* out) {
   const uint64_t nnz = rc.nnz;
+  const char* what = "duplicate check";
+  *out = ~0ull;
   if (nnz < 2) return SGDT_OK;
   KeyLayout kl{};
   uint32_t total = 0;
@@ -373,7 +414,7 @@ int check_duplicates(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d
       size_t need = 0;
       if (cub::DeviceRadixSort::SortPairs(nullptr, need, k_in, k_out, p_in, p_out, static_cast<int64_t>(nnz), 0,
                                           bits, s.stream) != cudaSuccess) {
-        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check (sort sizing) failed");
+        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": sort sizing failed");
         break;
       }
       if (need > tmp_bytes) {
@@ -381,14 +422,14 @@ int check_duplicates(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d
         tmp = nullptr;
         if (cudaMalloc(&tmp, need) != cudaSuccess) {
           cudaGetLastError();
-          rc_ = fail(SGDT_ERR_CONFIG, std::string(what) + ": out of device memory in the duplicate check");
+          rc_ = fail(SGDT_ERR_CONFIG, std::string(what) + ": out of device memory");
           break;
         }
         tmp_bytes = need;
       }
       if (cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, p_in, p_out, static_cast<int64_t>(nnz), 0,
                                           bits, s.stream) != cudaSuccess) {
-        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check (sort) failed");
+        rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": sort failed");
         break;
       }
       std::swap(p_in, p_out);
@@ -403,15 +444,14 @@ int check_duplicates(Session& s, const RecordCopy& rc, const sgdt_tensor_desc* d
         cudaMemcpyAsync(&h, first, sizeof h, cudaMemcpyDeviceToHost, s.stream) != cudaSuccess ||
         cudaStreamSynchronize(s.stream) != cudaSuccess) {
       cudaGetLastError();
-      rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + ": duplicate check failed");
+      rc_ = fail(SGDT_ERR_INTERNAL, std::string(what) + " failed");
     }
     s.launches += 2 + words;
   } while (false);
   for (void* p : {(void*)k_in, (void*)k_out, (void*)p_in, (void*)p_out, (void*)first, tmp})
     if (p) cudaFree(p);
   if (rc_) return rc_;
-  if (h != ~0ull)
-    return fail(SGDT_ERR_DATA, std::string(what) + ": entry " + std::to_string(h) + ": duplicate coordinate");
+  *out = h;
   return SGDT_OK;
 }
 
@@ -614,6 +654,9 @@ void free_session(sgdt_session* s) {
   for (cudaEvent_t e : {s->ev_start, s->ev_core, s->ev_samp})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->ev_copy)
+    if (e) cudaEventDestroy(e);
+  if (s->hx) cudaFreeHost(s->hx);
   if (s->side) cudaStreamDestroy(s->side);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -850,7 +893,16 @@ using namespace sgdt;
 extern "C" {
 
 const char* sgdt_last_error(void) { return g_error.c_str(); }
-const char* sgdt_version(void) { return "sgdt 0.1 (sm_100a)"; }
+const char* sgdt_version(void) { return "sgdt 0.2 (sm_100a)"; }
+
+int sgdt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 
 void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uint64_t* ends) {
   const uint64_t base = count / workers, rem = count % workers;
@@ -861,6 +913,88 @@ void sgdt_partition_even(uint64_t count, uint64_t workers, uint64_t* begins, uin
     ends[w] = at + len;
     at += len;
   }
+}
+
+__global__ void mode_key_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, int n, uint32_t* __restrict__ key) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    key[e] = idx[static_cast<uint64_t>(n) * nnz + e];
+}
+
+// off[r] = first position of bucket r in the sorted coordinates (0-based
+// rows; the host view is 1-based: offsets[i] = end of bucket i).
+__global__ void bucket_offsets_kernel(const uint32_t* __restrict__ keys, uint64_t len, uint32_t dim,
+                                      uint64_t* __restrict__ off) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q <= len;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cur = q < len ? static_cast<int64_t>(keys[q]) : static_cast<int64_t>(dim);
+    const int64_t prev = q > 0 ? static_cast<int64_t>(keys[q - 1]) : -1;
+    for (int64_t r = prev + 1; r <= cur; ++r) off[r] = q;
+  }
+}
+
+int sgdt_tensor_layout(const sgdt_tensor_desc* d, int device, uint32_t* const* perm_out,
+                       uint64_t* const* offsets_out) {
+  TRY(validate_desc(d, "tensor"));
+  if (device >= 0) SGDT_CUDA(cudaSetDevice(device));
+  Session tmp;
+  SGDT_CUDA(cudaGetDevice(&tmp.device));
+  SGDT_CUDA(cudaDeviceGetAttribute(&tmp.num_sms, cudaDevAttrMultiProcessorCount, tmp.device));
+  SGDT_CUDA(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking));
+  RecordCopy rc;
+  uint32_t *key = nullptr, *key2 = nullptr, *ids = nullptr, *ids2 = nullptr;
+  uint64_t* off = nullptr;
+  void* scratch = nullptr;
+  const uint64_t nnz = d->nnz;
+  int r = [&]() -> int {
+    TRY(upload_record_copy(tmp, d, rc, nullptr, nullptr));
+    TRY(check_entries(tmp, rc, d, ""));
+    if (!perm_out && !offsets_out) return SGDT_OK;
+    TRY(dalloc(&key, nnz));
+    TRY(dalloc(&key2, nnz));
+    TRY(dalloc(&ids, nnz));
+    TRY(dalloc(&ids2, nnz));
+    size_t cap = 0;
+    for (int n = 0; n < d->order; ++n) {
+      const uint32_t dim = d->dims[n];
+      int bits = 1;
+      while (bits < 32 && (1ull << bits) < dim) ++bits;
+      mode_key_kernel<<<grid_for(nnz, tmp.num_sms), 256, 0, tmp.stream>>>(rc.idx, nnz, n, key);
+      iota_u32_kernel<<<grid_for(nnz, tmp.num_sms), 256, 0, tmp.stream>>>(ids, nnz);
+      SGDT_CUDA(cudaGetLastError());
+      size_t need = 0;
+      SGDT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, ids, ids2, static_cast<int64_t>(nnz), 0,
+                                                bits, tmp.stream));
+      if (need > cap) {
+        if (scratch) cudaFree(scratch);
+        scratch = nullptr;
+        SGDT_CUDA(cudaMalloc(&scratch, need));
+        cap = need;
+      }
+      // stable: ids ascending inside each bucket (sptensor.cpp:102-117)
+      SGDT_CUDA(cub::DeviceRadixSort::SortPairs(scratch, cap, key, key2, ids, ids2, static_cast<int64_t>(nnz), 0,
+                                                bits, tmp.stream));
+      if (perm_out && perm_out[n])
+        SGDT_CUDA(cudaMemcpyAsync(perm_out[n], ids2, nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost, tmp.stream));
+      if (offsets_out && offsets_out[n]) {
+        if (off) cudaFree(off);
+        off = nullptr;
+        TRY(dalloc(&off, static_cast<uint64_t>(dim) + 1));
+        bucket_offsets_kernel<<<grid_for(nnz + 1, tmp.num_sms), 256, 0, tmp.stream>>>(key2, nnz, dim, off);
+        SGDT_CUDA(cudaGetLastError());
+        // host offsets[0] = 0, offsets[i] = end of bucket i (1-based rows)
+        SGDT_CUDA(cudaMemcpyAsync(offsets_out[n], off, (static_cast<uint64_t>(dim) + 1) * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, tmp.stream));
+      }
+      SGDT_CUDA(cudaStreamSynchronize(tmp.stream));
+    }
+    return SGDT_OK;
+  }();
+  for (void* p : {(void*)rc.idx, (void*)rc.val, (void*)key, (void*)key2, (void*)ids, (void*)ids2, (void*)off, scratch})
+    if (p) cudaFree(p);
+  cudaStreamDestroy(tmp.stream);
+  tmp.stream = nullptr;
+  return r;
 }
 
 int sgdt_session_create(const sgdt_tensor_desc* train, const sgdt_tensor_desc* test, const uint32_t* J,
@@ -925,8 +1059,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     }
     // records: entry order (kept for Psi gathers + train RMSE) and per mode
     TRY(upload_record_copy(*s, train, s->train_rec, nullptr, nullptr));
-    TRY(check_coords(*s, s->train_rec, train, "train"));
-    TRY(check_duplicates(*s, s->train_rec, train, "train"));
+    TRY(check_entries(*s, s->train_rec, train, "train: "));
     uint32_t max_pieces = 0;
     std::vector<uint64_t> off;
     std::vector<uint32_t> perm;
@@ -992,8 +1125,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     if (test) {
       s->nnz_test = test->nnz;
       TRY(upload_record_copy(*s, test, s->test_rec, nullptr, nullptr));
-      TRY(check_coords(*s, s->test_rec, test, "test"));
-      TRY(check_duplicates(*s, s->test_rec, test, "test"));
+      TRY(check_entries(*s, s->test_rec, test, "test: "));
     }
     // model
     uint64_t stage = 0;
@@ -1069,17 +1201,22 @@ int sgdt_set_model(sgdt_session* s, const double* const* A, const double* const*
 }
 
 int sgdt_get_model(sgdt_session* s, double* const* A, double* const* B) {
-  if (!s || !A || !B) return fail(SGDT_ERR_DOMAIN, "get_model: null argument");
+  if (!s || (!A && !B)) return fail(SGDT_ERR_DOMAIN, "get_model: null argument");
   SGDT_CUDA(cudaSetDevice(s->device));
   for (int k = 0; k < s->order; ++k) {
     const uint64_t na = static_cast<uint64_t>(s->dims[k]) * s->J[k];
     const uint64_t nb = static_cast<uint64_t>(s->J[k]) * s->R;
-    cast_f2d_kernel<<<grid_for(na, s->num_sms), 256, 0, s->stream>>>(s->P.A[k], s->stage, na);
-    SGDT_CUDA(cudaMemcpyAsync(A[k], s->stage, na * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    cast_f2d_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->P.B[k], s->stage, nb);
-    SGDT_CUDA(cudaMemcpyAsync(B[k], s->stage, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    if (A) {
+      cast_f2d_kernel<<<grid_for(na, s->num_sms), 256, 0, s->stream>>>(s->P.A[k], s->stage, na);
+      SGDT_CUDA(cudaMemcpyAsync(A[k], s->stage, na * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      ++s->launches;
+    }
+    if (B) {
+      cast_f2d_kernel<<<grid_for(nb, s->num_sms), 256, 0, s->stream>>>(s->P.B[k], s->stage, nb);
+      SGDT_CUDA(cudaMemcpyAsync(B[k], s->stage, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      ++s->launches;
+    }
     SGDT_CUDA(cudaGetLastError());
-    s->launches += 2;
   }
   SGDT_CUDA(cudaStreamSynchronize(s->stream));
   return SGDT_OK;
@@ -1145,6 +1282,7 @@ int sgdt_sample_batch(sgdt_session* s, uint64_t m, uint32_t* out) {
   if (m < 1 || m > s->nnz) return fail(SGDT_ERR_DOMAIN, "sample_batch: batch size out of range");
   SGDT_CUDA(cudaSetDevice(s->device));
   TRY(settle_ahead(*s, false, "sample_batch"));
+  s->delta_base = s->sampler_runs;
   TRY(ensure_batch_capacity(*s, m));
   TRY(launch_sampler(*s, m, s->batch, s->stream));
   if (out) SGDT_CUDA(cudaMemcpyAsync(out, s->batch, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
@@ -1169,6 +1307,7 @@ int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* 
   uint64_t m = 0;
   TRY(check_core_hyper(*s, h, &m));
   SGDT_CUDA(cudaSetDevice(s->device));
+  s->delta_base = s->sampler_runs;
   if (st) {
     st->batch_size = h->lr == 0.0 ? 0 : m;
     st->effective_workers = h->lr == 0.0 ? 0 : 1;
@@ -1194,6 +1333,94 @@ int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_s
   if (h->lr == 0.0) return SGDT_OK;
   if (h->row_fraction < 1.0) TRY(settle_ahead(*s, false, "factor_epoch (row_fraction < 1)"));
   TRY(enqueue_factor(*s, *h, false));
+  return sync_and_flag(*s);
+}
+
+__global__ void pool_delta_kernel(const uint32_t* __restrict__ draw_j, const uint32_t* __restrict__ pool, uint64_t m,
+                                  uint32_t* pos, uint32_t* val) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = draw_j[i];
+    pos[i] = p;
+    val[i] = pool[p];
+  }
+}
+
+int sgdt_pool_delta(sgdt_session* s, uint32_t* pos, uint32_t* val, uint64_t* n) {
+  if (!s || !pos || !val || !n) return fail(SGDT_ERR_DOMAIN, "pool_delta: null argument");
+  if (s->ahead_valid || s->sampler_runs != s->delta_base + 1)
+    return fail(SGDT_ERR_CONFIG, "pool_delta: the last call did not make exactly one sampler run");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  const uint64_t m = s->delta_m;
+  uint32_t* d = nullptr;
+  TRY(dalloc(&d, 2 * m));
+  pool_delta_kernel<<<grid_for(m, s->num_sms), 256, 0, s->stream>>>(s->draw_j, s->pool, m, d, d + m);
+  ++s->launches;
+  int rc = SGDT_OK;
+  if (cudaGetLastError() != cudaSuccess ||
+      cudaMemcpyAsync(pos, d, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+      cudaMemcpyAsync(val, d + m, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+      cudaStreamSynchronize(s->stream) != cudaSuccess) {
+    cudaGetLastError();
+    rc = fail(SGDT_ERR_INTERNAL, "pool_delta: copy failed");
+  }
+  cudaFree(d);
+  *n = rc == SGDT_OK ? m : 0;
+  return rc;
+}
+
+int sgdt_factor_epoch_host(sgdt_session* s, const sgdt_factor_hyper* h, double* const* A_out, sgdt_factor_stats* st) {
+  if (!s || !A_out) return fail(SGDT_ERR_DOMAIN, "factor_epoch_host: null argument");
+  TRY(check_factor_hyper(h));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  if (st) {
+    *st = sgdt_factor_stats{0, 0, 0.0};
+    if (h->lr > 0.0)
+      for (int n = 0; n < s->order; ++n) {
+        st->rows_updated += s->mode[n].rows_nonempty;
+        st->rows_skipped += s->mode[n].rows_empty;
+      }
+  }
+  if (h->lr == 0.0) return SGDT_OK;  // A unchanged: nothing to copy
+  if (h->row_fraction < 1.0) TRY(settle_ahead(*s, false, "factor_epoch_host (row_fraction < 1)"));
+  uint64_t off[kMaxOrder + 1] = {0};
+  for (int k = 0; k < s->order; ++k) off[k + 1] = off[k] + static_cast<uint64_t>(s->dims[k]) * s->J[k];
+  if (off[s->order] > s->xfer_cap) {
+    if (s->xfer) cudaFree(s->xfer);
+    s->xfer = nullptr;
+    s->xfer_cap = 0;
+    TRY(dalloc(&s->xfer, off[s->order]));
+    s->xfer_cap = off[s->order];
+  }
+  if (off[s->order] > s->hx_cap) {
+    if (s->hx) cudaFreeHost(s->hx);
+    s->hx = nullptr;
+    s->hx_cap = 0;
+    SGDT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->hx), off[s->order] * sizeof(double), cudaHostAllocDefault));
+    s->hx_cap = off[s->order];
+  }
+  for (int n = 0; n < s->order; ++n)
+    if (!s->ev_copy[n]) SGDT_CUDA(cudaEventCreateWithFlags(&s->ev_copy[n], cudaEventDisableTiming));
+  // the factor passes; ev[4 + n] marks the start of mode n, ev[2] the end
+  TRY(enqueue_factor(*s, *h, true));
+  SGDT_CUDA(cudaEventRecord(s->ev[2], s->stream));
+  // A^(n) is final once mode n's pass is done: cast + D2H on the side stream
+  // while the later modes run, then the host copies it out of the pinned
+  // staging while the GPU is still busy
+  for (int n = 0; n < s->order; ++n) {
+    SGDT_CUDA(cudaStreamWaitEvent(s->side, n + 1 < s->order ? s->ev[4 + n + 1] : s->ev[2], 0));
+    const uint64_t na = off[n + 1] - off[n];
+    cast_f2d_kernel<<<grid_for(na, s->num_sms), 256, 0, s->side>>>(s->P.A[n], s->xfer + off[n], na);
+    SGDT_CUDA(cudaMemcpyAsync(s->hx + off[n], s->xfer + off[n], na * sizeof(double), cudaMemcpyDeviceToHost,
+                              s->side));
+    SGDT_CUDA(cudaEventRecord(s->ev_copy[n], s->side));
+    ++s->launches;
+  }
+  SGDT_CUDA(cudaGetLastError());
+  for (int n = 0; n < s->order; ++n) {
+    SGDT_CUDA(cudaEventSynchronize(s->ev_copy[n]));
+    parallel_copy(A_out[n], s->hx + off[n], (off[n + 1] - off[n]) * sizeof(double));
+  }
   return sync_and_flag(*s);
 }
 

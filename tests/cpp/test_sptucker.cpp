@@ -340,6 +340,75 @@ void test_train_end_to_end_vs_oracle() {
   CHECK(ident);
 }
 
+// Device residency of the per-epoch calls: with no host edits in between,
+// K epochs through update_core_epoch / update_factor_epoch (model and pool
+// kept on the device, B / A / pool deltas copied back) equal train()'s
+// device loop bit for bit, and the host workspace pool equals the oracle's;
+// host edits between calls (a factor row, a Kruskal column, two pool slots)
+// are seen and uploaded.
+void test_resident_per_epoch_calls() {
+  const std::vector<std::uint32_t> dims{60, 300, 40}, J{8, 8, 8};
+  const double sig = unit_sigma(3, 8, 8);
+  const Data d = planted(dims, J, 8, 20000, 0.05, 0.0, sig, 5);
+  const CooTensor t = to_tensor(d);
+  HyperParams h;
+  h.ranks = J;
+  h.r_core = 8;
+  h.lr_a = h.lr_b = 0.01;
+  h.reg_a = h.reg_b = 0.01;
+  h.batch_m = 1024;
+  h.epochs = 3;
+  h.seed = 4;
+  h.init_mean = 0.0;
+  h.init_stddev = sig;
+  auto [want, res] = train_from_scratch(t, nullptr, h);
+  TuckerModel tm = TuckerModel::init_gaussian(t.shape(), Ranks{J, 8}, 0.0, sig, h.seed);
+  Rng rng(h.seed + 1);
+  CoreBatchWorkspace ws;
+  std::vector<RowBatchWorkspace> rws;
+  SchedContext sched;
+  OTensor ot(d);
+  or_core_ws ows;
+  or_core_ws_init(&ows, t.nnz());
+  or_rng orng;
+  copy_rng(rng, orng);
+  for (std::size_t e = 0; e < h.epochs; ++e) {
+    update_core_epoch(tm, t, CoreHyper{h.lr_b, h.reg_b, h.batch_m, false, false}, sched, rng, ws);
+    update_factor_epoch(tm, t, FactorHyper{h.lr_a, h.reg_a, 1.0}, sched, rng, rws);
+    // the oracle's sampler alone tracks the pool (no model needed for Psi)
+    std::vector<std::uint32_t> psi(h.batch_m);
+    or_sample_batch(t.nnz(), h.batch_m, &orng, ows.pool, &ows.pool_valid, psi.data());
+    CHECK(std::equal(psi.begin(), psi.end(), ws.batch.begin()));
+    CHECK(std::equal(ws.sample_pool.begin(), ws.sample_pool.end(), ows.pool));
+  }
+  bool ident = true;
+  for (std::size_t n = 0; n < 3; ++n) ident &= tm.factor(n) == want.factor(n) && tm.kruskal(n) == want.kruskal(n);
+  CHECK(ident);
+  // host edits between calls: a factor entry, a Kruskal entry, two pool slots
+  tm.factor(1).at(7, 3) += 0.25;
+  tm.kruskal(2).at(1, 1) -= 0.125;
+  tm.refresh_core_cache();
+  std::swap(ws.sample_pool[3], ws.sample_pool[t.nnz() - 2]);
+  std::swap(ows.pool[3], ows.pool[t.nnz() - 2]);
+  TuckerModel edited = tm;
+  CoreBatchWorkspace ws2;
+  ws2.sample_pool = ws.sample_pool;
+  Rng rng2 = rng;
+  update_core_epoch(tm, t, CoreHyper{h.lr_b, h.reg_b, h.batch_m, false, false}, sched, rng, ws);
+  std::vector<std::uint32_t> psi(h.batch_m);
+  or_sample_batch(t.nnz(), h.batch_m, &orng, ows.pool, &ows.pool_valid, psi.data());
+  CHECK(std::equal(psi.begin(), psi.end(), ws.batch.begin()));
+  CHECK(std::equal(ws.sample_pool.begin(), ws.sample_pool.end(), ows.pool));
+  // the same step on a fresh tensor object (new device session: everything
+  // uploaded) gives the identical B
+  const CooTensor t2 = to_tensor(d);
+  update_core_epoch(edited, t2, CoreHyper{h.lr_b, h.reg_b, h.batch_m, false, false}, sched, rng2, ws2);
+  bool same = ws2.batch == ws.batch;
+  for (std::size_t n = 0; n < 3; ++n) same &= edited.kruskal(n) == tm.kruskal(n) && edited.factor(n) == tm.factor(n);
+  CHECK(same);
+  or_core_ws_free(&ows);
+}
+
 void test_config_errors() {
   const Data d = planted({12, 10, 8}, {3, 3, 3}, 3, 300, 0.02, 0.5, 0.1, 2);
   const CooTensor t = to_tensor(d);
@@ -628,6 +697,7 @@ int main(int argc, char** argv) {
   run("rmse", test_rmse_fixed_and_perfect);
   run("freeze and errors", test_freeze_and_errors);
   run("train end to end", test_train_end_to_end_vs_oracle);
+  run("resident per-epoch calls", test_resident_per_epoch_calls);
   run("config errors", test_config_errors);
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -32,6 +32,8 @@ API = [
     "sptucker::TuckerModel::save(", "sptucker::TuckerModel::load(", "sptucker::write_metrics_csv(",
     "sptucker::parse_metrics_csv(", "sptucker::synth_planted(", "sptucker::synth_ratings(",
     "sptucker::unfold_col_index(", "sptucker::vec_index(", "sptucker::invert_vec_index(",
+    # the reference's epoch benches (eval.hpp:53-95)
+    "sptucker::bench_rank_scaling(", "sptucker::bench_speedup(", "sptucker::fit_linear(",
 ]
 GOLDEN_IO = os.path.join(ROOT, "tests", "golden", "io")
 
