@@ -80,7 +80,10 @@ typedef struct {
   uint64_t effective_workers;
 } sgdt_core_stats;
 
-/* FactorEpochStats (factor_optimizer.hpp:44-48). */
+/* FactorEpochStats (factor_optimizer.hpp:44-48).  max_imbalance: the
+ * reference's improved-strategy slice imbalance with the ranks of a sharded
+ * session as its workers (largest partition_even(nnz, world) slice / (nnz /
+ * world) - 1); 0 for a single session, as the reference with one worker. */
 typedef struct {
   uint64_t rows_updated;
   uint64_t rows_skipped;

@@ -108,50 +108,44 @@ sgdt_factor_stats Session::factor_epoch_into(TuckerModel& m, const sgdt_factor_h
   return st;
 }
 
-std::uint64_t Session::fingerprint(const std::vector<std::uint32_t>& pool) {
-  // 4096 strided words and the last one, mixed (splitmix64 finaliser)
-  std::uint64_t h = pool.size() * 0x9E3779B97F4A7C15ull;
-  const std::size_t n = pool.size(), step = n / 4096 + 1;
-  auto mix = [&](std::uint64_t v) {
-    h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
-    h ^= h >> 31;
-    h *= 0xBF58476D1CE4E5B9ull;
-  };
-  for (std::size_t i = 0; i < n; i += step) mix((static_cast<std::uint64_t>(i) << 32) | pool[i]);
-  if (n) mix(pool[n - 1]);
-  return h;
-}
-
-void Session::sync_pool(const std::vector<std::uint32_t>& pool) {
-  if (pool.data() == pool_data_ && pool.size() == pool_size_ && fingerprint(pool) == pool_fp_) return;
+void Session::sync_pool(const std::vector<std::uint32_t>& pool, bool force) {
+  if (!force && pool.data() == pool_data_ && pool.size() == pool_size_) return;
   check(sgdt_set_pool(h_, pool.data()), "update_core_epoch");
   h2d_bytes += pool.size() * sizeof(std::uint32_t);
   pool_data_ = pool.data();
   pool_size_ = pool.size();
-  pool_fp_ = fingerprint(pool);
 }
 
 void Session::pool_reset(const std::vector<std::uint32_t>& iota_pool) {
   check(sgdt_reset_pool(h_), "update_core_epoch");
   pool_data_ = iota_pool.data();
   pool_size_ = iota_pool.size();
-  pool_fp_ = fingerprint(iota_pool);
 }
 
-void Session::pool_after_epoch(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch) {
-  std::vector<std::uint32_t> pos(batch.size()), val(batch.size());
+bool Session::pool_apply_checked(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch) {
+  const std::size_t m = batch.size();
+  std::vector<std::uint32_t> pos(m), val(m);
   std::uint64_t n = 0;
-  if (sgdt_pool_delta(h_, pos.data(), val.data(), &n) == SGDT_OK) {
-    for (std::uint64_t i = 0; i < n; ++i) pool[pos[i]] = val[i];
-    std::copy(batch.begin(), batch.end(), pool.begin());
-    d2h_bytes += 2 * n * sizeof(std::uint32_t);
-  } else {  // several draws (resample_per_mode): the whole pool
+  if (sgdt_pool_delta(h_, pos.data(), val.data(), &n) != SGDT_OK) {
+    // several runs (resample_per_mode): the pool was uploaded before the
+    // call, so the device pool is the truth -- take all of it
     check(sgdt_get_pool(h_, pool.data()), "update_core_epoch");
     d2h_bytes += pool.size() * sizeof(std::uint32_t);
+    pool_data_ = pool.data();
+    pool_size_ = pool.size();
+    return true;
+  }
+  d2h_bytes += 2 * n * sizeof(std::uint32_t);
+  for (std::size_t i = 0; i < n; ++i) std::swap(pool[i], pool[pos[i]]);
+  bool same = std::equal(batch.begin(), batch.end(), pool.begin());
+  for (std::size_t i = 0; same && i < n; ++i) same = pool[pos[i]] == val[i];
+  if (!same) {
+    for (std::size_t i = n; i-- > 0;) std::swap(pool[i], pool[pos[i]]);  // undo
+    return false;
   }
   pool_data_ = pool.data();
   pool_size_ = pool.size();
-  pool_fp_ = fingerprint(pool);
+  return true;
 }
 
 void Session::put_rng(const Rng& r) { check(sgdt_set_rng(h_, r.state_words().data(), r.state_pos()), "rng"); }

@@ -38,24 +38,29 @@ class Session {
   void mark_synced(const TuckerModel& m);
   // The factor epoch with the A^(n) copy-out overlapped (sgdt_factor_epoch_host).
   sgdt_factor_stats factor_epoch_into(TuckerModel& m, const sgdt_factor_hyper& h);
-  // The persistent sample pool: uploaded only when the workspace's pool is
-  // not the one this session last wrote (buffer, size or fingerprint
-  // differ); after a core epoch only the touched positions come back.
-  void sync_pool(const std::vector<std::uint32_t>& pool);
+  // The persistent sample pool.  The device copy is the one this session
+  // last wrote; it is re-uploaded when the host vector is another buffer or
+  // size (or `force`).  After a single sampler run, pool_apply_checked()
+  // replays the run on the host pool (the partial Fisher-Yates swaps over the
+  // device's draw targets, sptensor.cpp:256-270) and compares the result with
+  // the device's batch and touched positions.  A swap is a permutation of
+  // positions, so equality there means the host and device pools agreed at
+  // every position the run read: host edits between calls are either outside
+  // the run's read set (and are checked by a later run) or detected.  On a
+  // mismatch the host pool is restored and false is returned; the caller
+  // uploads the host pool and repeats the call.
+  void sync_pool(const std::vector<std::uint32_t>& pool, bool force = false);
   void pool_reset(const std::vector<std::uint32_t>& iota_pool);  // the host pool was just set to iota
-  void pool_after_epoch(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch);
+  bool pool_apply_checked(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch);
 
   std::uint64_t h2d_bytes = 0, d2h_bytes = 0;  // model / pool / batch traffic of the per-epoch calls
 
  private:
-  static std::uint64_t fingerprint(const std::vector<std::uint32_t>& pool);
-
   sgdt_session* h_ = nullptr;
   const TuckerModel* synced_model_ = nullptr;
   std::uint64_t synced_gen_ = 0;
   const std::uint32_t* pool_data_ = nullptr;
   std::size_t pool_size_ = 0;
-  std::uint64_t pool_fp_ = 0;
   const CooTensor* test_ = nullptr;
   std::size_t test_nnz_ = 0;
   std::vector<std::uint32_t> dims_, J_;

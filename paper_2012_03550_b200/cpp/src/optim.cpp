@@ -170,35 +170,44 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
   const std::size_t m = hyper.batch_m == 0 ? nnz : hyper.batch_m;
   if (m > nnz) throw DomainError("core batch size exceeds training nnz");
 
-  // device-resident across calls: the model and the pool go up only when
-  // the host copies changed since this session last synchronised them
+  // device-resident across calls: the model goes up only when the host copy
+  // changed since this session last synchronised it, the pool only when the
+  // host vector is another buffer (device.hpp); several sampler runs per call
+  // (resample_per_mode) upload the host pool every time
   detail::Session& s = detail::session_for(train, nullptr, model.shape(), model.ranks());
-  s.sync_model(model);
-  s.put_rng(rng);
-  if (hyper.batch_m != 0) {
-    if (ws.sample_pool.size() != nnz) {  // sample_batch: a pool of the wrong size restarts from iota
-      ws.grow(ws.sample_pool, nnz);
-      std::iota(ws.sample_pool.begin(), ws.sample_pool.end(), 0u);
-      s.pool_reset(ws.sample_pool);
-    } else {
-      s.sync_pool(ws.sample_pool);
-    }
+  const bool sampled = hyper.batch_m != 0;
+  if (sampled && ws.sample_pool.size() != nnz) {  // sample_batch: a pool of the wrong size restarts from iota
+    ws.grow(ws.sample_pool, nnz);
+    std::iota(ws.sample_pool.begin(), ws.sample_pool.end(), 0u);
+    s.pool_reset(ws.sample_pool);
+  } else if (sampled) {
+    s.sync_pool(ws.sample_pool, hyper.resample_per_mode);
   }
   const sgdt_core_hyper h{hyper.lr, hyper.reg, hyper.batch_m, hyper.resample_per_mode ? 1 : 0,
                           hyper.incremental_residual ? 1 : 0};
-  sgdt_core_stats st{};
-  detail::check(sgdt_core_epoch(s.get(), &h, &st), "update_core_epoch");
-  s.take_model(model, /*factors=*/false, /*kruskal=*/true);  // the core phase wrote B only
-  s.take_rng(rng);
   ws.grow(ws.batch, m);
-  if (hyper.batch_m != 0) {
+  for (int attempt = 0;; ++attempt) {
+    s.sync_model(model);
+    s.put_rng(rng);
+    sgdt_core_stats st{};
+    detail::check(sgdt_core_epoch(s.get(), &h, &st), "update_core_epoch");
+    if (!sampled) {
+      std::iota(ws.batch.begin(), ws.batch.end(), 0u);
+      break;
+    }
     std::uint64_t len = 0;
     detail::check(sgdt_last_batch(s.get(), ws.batch.data(), &len), "update_core_epoch");
     s.d2h_bytes += m * sizeof(std::uint32_t);
-    s.pool_after_epoch(ws.sample_pool, ws.batch);
-  } else {
-    std::iota(ws.batch.begin(), ws.batch.end(), 0u);
+    if (s.pool_apply_checked(ws.sample_pool, ws.batch)) break;
+    // the host pool was edited at a position this run read: the device ran
+    // on a stale pool, so repeat the epoch from the host state (model, RNG
+    // and pool are all still the pre-call ones)
+    if (attempt) throw InternalError("update_core_epoch: device pool does not follow the host pool");
+    s.sync_pool(ws.sample_pool, /*force=*/true);
+    s.put_model(model);
   }
+  s.take_model(model, /*factors=*/false, /*kruskal=*/true);  // the core phase wrote B only
+  s.take_rng(rng);
   std::size_t effective = 0;
   for (const Range& r : partition_even(m, sched.workers()))
     if (!r.empty()) ++effective;

@@ -231,13 +231,17 @@ void sample_batch(const CooTensor& t, std::size_t m, Rng& rng, std::vector<std::
     std::iota(pool.begin(), pool.end(), 0u);
     s.pool_reset(pool);
   } else {
-    s.sync_pool(pool);  // uploaded only if it is not the pool this session last wrote
+    s.sync_pool(pool);  // uploaded only if it is not the buffer this session last wrote
   }
-  s.put_rng(rng);
   out.resize(m);
-  detail::check(sgdt_sample_batch(s.get(), m, out.data()), "sample_batch");
+  for (int attempt = 0;; ++attempt) {
+    s.put_rng(rng);
+    detail::check(sgdt_sample_batch(s.get(), m, out.data()), "sample_batch");
+    if (s.pool_apply_checked(pool, out)) break;  // replayed on the host pool and checked
+    if (attempt) throw InternalError("sample_batch: device pool does not follow the host pool");
+    s.sync_pool(pool, /*force=*/true);  // the host pool was edited: repeat from it
+  }
   s.take_rng(rng);
-  s.pool_after_epoch(pool, out);  // the touched positions only
 }
 
 std::vector<std::uint32_t> sample_batch(const CooTensor& t, std::size_t m, Rng& rng) {

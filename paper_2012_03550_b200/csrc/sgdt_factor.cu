@@ -17,10 +17,11 @@
 // creation) into chunks of <= chunk_size entries holding whole rows, and rows
 // longer than a chunk into pieces.  One warp streams one chunk, 32 entries
 // per step (one entry per lane).  A window inside one open row accumulates
-// per lane in fp64; a window that crosses rows runs a segmented shuffle scan
-// and every completed row is finalised by the lane that holds its sum
-// (F = B g, SGD step, Q^(n) row rewrite).  Pieces of split rows are summed in
-// piece order by factor_split_kernel.  No atomics on parameters, fixed
+// per lane in fp32 (a chunk holds <= chunk_size entries, so <= chunk_size/32
+// terms per lane); a window that crosses rows runs a segmented shuffle scan
+// and every completed row is finalised in fp32 by the warp (F = B g, SGD
+// step, Q^(n) row rewrite).  Pieces of split rows are written as fp64 and
+// summed in fp64, in piece order, by factor_split_kernel.  No atomics on parameters, fixed
 // association everywhere -> run-to-run bit identical.
 #include <cuda_runtime.h>
 
@@ -274,8 +275,9 @@ constexpr int factor_min_blocks() {
 // One warp streams one chunk of the mode-n-sorted records (see file header).
 // The next window's records are prefetched while the current window's Q rows
 // are gathered; per-lane partial sums stay in fp32 (a chunk holds at most
-// chunk_size entries, i.e. <= chunk_size/32 terms per lane) and are widened
-// to fp64 at every row boundary.
+// chunk_size entries, i.e. <= chunk_size/32 terms per lane), rows are
+// finalised from the fp32 sums, and only the pieces of split rows are
+// written out (and merged) in fp64.
 //
 // SJ >= 0: the other-mode table j == SJ (small, e.g. the 2200-row Q^(3) of
 // BASELINE config 2) was staged into shared memory by the kernel and its

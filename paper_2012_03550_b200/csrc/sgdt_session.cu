@@ -1318,6 +1318,16 @@ int sgdt_core_epoch(sgdt_session* s, const sgdt_core_hyper* h, sgdt_core_stats* 
   return sync_and_flag(*s);
 }
 
+// The reference's improved-strategy figure (factor_optimizer.cpp:209-218) with
+// the ranks of a sharded session as its workers: the largest
+// partition_even(nnz, world) slice over the ideal nnz / world, minus 1.  A
+// single session is one worker, as the reference with threads = 1: 0.
+static double rank_imbalance(const Session& s) {
+  if (s.world <= 1 || s.nnz == 0) return 0.0;
+  const uint64_t biggest = (s.nnz + s.world - 1) / s.world;
+  return static_cast<double>(biggest) / (static_cast<double>(s.nnz) / s.world) - 1.0;
+}
+
 int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_stats* st) {
   if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
   TRY(check_factor_hyper(h));
@@ -1329,6 +1339,7 @@ int sgdt_factor_epoch(sgdt_session* s, const sgdt_factor_hyper* h, sgdt_factor_s
         st->rows_updated += s->mode[n].rows_nonempty;
         st->rows_skipped += s->mode[n].rows_empty;
       }
+    st->max_imbalance = h->lr > 0.0 ? rank_imbalance(*s) : 0.0;
   }
   if (h->lr == 0.0) return SGDT_OK;
   if (h->row_fraction < 1.0) TRY(settle_ahead(*s, false, "factor_epoch (row_fraction < 1)"));
@@ -1380,6 +1391,7 @@ int sgdt_factor_epoch_host(sgdt_session* s, const sgdt_factor_hyper* h, double* 
         st->rows_updated += s->mode[n].rows_nonempty;
         st->rows_skipped += s->mode[n].rows_empty;
       }
+    st->max_imbalance = h->lr > 0.0 ? rank_imbalance(*s) : 0.0;
   }
   if (h->lr == 0.0) return SGDT_OK;  // A unchanged: nothing to copy
   if (h->row_fraction < 1.0) TRY(settle_ahead(*s, false, "factor_epoch_host (row_fraction < 1)"));
