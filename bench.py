@@ -419,7 +419,7 @@ def run_sharded(args, rank, world, local_rank):
     fh = sgdt.FactorHyper(HYPER["lr_a"], HYPER["reg_a"], 1.0)
     D.connect_peers(s, group)
     dist.barrier()
-    D.run_epochs_p2p(s, group, ch, fh, args.warmup)
+    D.run_epochs_p2p(s, group, ch, fh, args.warmup, core=args.core)
     stream = torch.cuda.ExternalStream(s.stream)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -428,7 +428,7 @@ def run_sharded(args, rank, world, local_rank):
     launches0 = s.launch_count()
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
-        D.run_epochs_p2p(s, group, ch, fh, args.steps)
+        D.run_epochs_p2p(s, group, ch, fh, args.steps, core=args.core)
         ev1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
@@ -449,14 +449,14 @@ def run_sharded(args, rank, world, local_rank):
         d2h = sum(a.nbytes for a in oA) + sum(b.nbytes for b in oB)
         for _ in range(args.warmup):  # untimed
             s.set_model(hA, hB)
-            D.run_epochs_p2p(s, group, ch, fh, 1)
+            D.run_epochs_p2p(s, group, ch, fh, 1, core=args.core)
             s.get_model((oA, oB))
         dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             s.set_model(hA, hB)
-            D.run_epochs_p2p(s, group, ch, fh, 1)
+            D.run_epochs_p2p(s, group, ch, fh, 1, core=args.core)
             s.get_model((oA, oB))
             hA, oA = oA, hA
             hB, oB = oB, hB

@@ -266,16 +266,40 @@ int sgdt_synchronize(sgdt_session* s);
  * sgdt_factor_mode_p2p and after sgdt_factor_merge_p2p (a stream-ordered
  * collective or a host barrier after sgdt_synchronize). */
 
-/* This session's peer-visible buffers, 2N+1 device pointers: A^(0..N-1),
- * Q^(0..N-1), the export-record slots. */
+/* This session's peer-visible buffers, 2N+2 device pointers: A^(0..N-1),
+ * Q^(0..N-1), the export-record slots, the core-phase exchange buffer
+ * (sgdt_core_plan). */
 int sgdt_peer_buffers(sgdt_session* s, void** ptrs);
-/* The same buffers as CUDA IPC handles (2N+1 x 64 bytes), for peers in other
+/* The same buffers as CUDA IPC handles (2N+2 x 64 bytes), for peers in other
  * processes; sgdt_ipc_open maps one into the calling process. */
 int sgdt_peer_ipc_handles(sgdt_session* s, void* handles);
 int sgdt_ipc_open(const void* handle, int device, void** ptr);
-/* Install every rank's buffers: ptrs is world x (2N+1) pointers valid in this
+/* Install every rank's buffers: ptrs is world x (2N+2) pointers valid in this
  * process, rank-major (this rank's own row is ignored). */
 int sgdt_set_peers(sgdt_session* s, const void* const* ptrs);
+/* ---- sharded core phase (update_core_epoch, core_optimizer.cpp:112-257,
+ * with Psi sliced by partition_even(M, world) over the ranks as the
+ * reference slices it over workers, scheduler.cpp:34-46, and the per-worker
+ * partials merged in rank order, core_optimizer.cpp:225-243) -------------
+ * The columns of B^(n) are taken in blocks of T.  Per block every rank
+ * reduces, over its Psi slice, V0_r = sum_s c_{s,r} (xhat_s - x_s) a_s and
+ * G_{r,r'} = sum_s c_{s,r} c_{s,r'} a_s a_s^T for the block's columns, and
+ * stores that vector into slot `rank` of every rank's exchange buffer (P2P
+ * stores); the next step sums the slots in rank order and replays the T
+ * Gauss-Seidel column steps identically on every rank.  So the only
+ * cross-GPU traffic of the core phase is these B^(n)-gradient vectors,
+ * N * ceil(R/T) per epoch.  Usage:
+ *   steps = sgdt_core_plan(...);
+ *   for k < steps: sgdt_core_step(s, k); if k + 1 < steps: barrier over ranks
+ * (the barrier: a stream-ordered collective, or sgdt_synchronize + a host
+ * barrier).  With world = 1 no barrier is needed; sgdt_core_plan draws Psi
+ * (or consumes a pending sgdt_sample_ahead) exactly as sgdt_core_epoch_async.
+ * *steps = 0 for lr = 0 (a frozen phase, no RNG).  `block` = 0 picks T from
+ * a cost model (SGDT_CORE_T overrides); *T_out receives it. */
+int sgdt_core_plan(sgdt_session* s, const sgdt_core_hyper* h, uint32_t block, uint32_t* steps,
+                   uint32_t* T_out);
+int sgdt_core_step(sgdt_session* s, uint32_t k);
+
 /* Replicated core phase without a host synchronisation (the numeric flag is
  * checked by sgdt_check). */
 int sgdt_core_epoch_async(sgdt_session* s, const sgdt_core_hyper* h);
@@ -293,6 +317,17 @@ int sgdt_factor_mode_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h);
  * records and the owner's finalisation of the cut row it publishes (peer
  * stores included).  Asynchronous. */
 int sgdt_factor_merge_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h);
+/* Peer access between the devices of a group driven by one process
+ * (cudaDeviceEnablePeerAccess for every ordered pair of distinct devices;
+ * pairs already enabled are fine).  SGDT_ERR_CONFIG when a pair has no P2P. */
+int sgdt_enable_peer_access(const int* devices, int n);
+/* Stream-ordered barrier over sessions held by one process: each session's
+ * stream waits (cudaStreamWaitEvent, across devices) for the work enqueued so
+ * far on every other session's stream.  No host synchronisation, and no
+ * kernel ever waits on another: the ordering is the streams'.  This is the
+ * barrier of the C++ multi-GPU train() (one host thread enqueues every rank
+ * in lockstep). */
+int sgdt_stream_barrier(sgdt_session* const* sessions, int n);
 /* Synchronise and check the numeric flag (SGDT_ERR_NUMERIC on divergence). */
 int sgdt_check(sgdt_session* s);
 

@@ -19,7 +19,6 @@ void throw_for(int code, const std::string& where) {
   }
 }
 
-namespace {
 sgdt_tensor_desc describe(const CooTensor& t, const std::vector<std::uint32_t>& dims,
                           std::vector<const std::uint32_t*>& perms) {
   perms.resize(t.order());
@@ -34,6 +33,7 @@ sgdt_tensor_desc describe(const CooTensor& t, const std::vector<std::uint32_t>& 
   return d;
 }
 
+namespace {
 std::uint64_t model_bytes(const TuckerModel& m, bool factors, bool kruskal) {
   std::uint64_t b = 0;
   for (std::size_t n = 0; n < m.order(); ++n)

@@ -73,6 +73,20 @@ struct DeviceCache {
   std::vector<std::unique_ptr<Session>> sessions;
 };
 
+// The C-ABI descriptor of a tensor (perms receives the per-mode orders).
+sgdt_tensor_desc describe(const CooTensor& t, const std::vector<std::uint32_t>& dims,
+                          std::vector<const std::uint32_t*>& perms);
+
+}  // namespace sptucker::detail
+namespace sptucker {
+struct HyperParams;
+struct TrainResult;
+}  // namespace sptucker
+namespace sptucker::detail {
+// train() over HyperParams::devices (multi_gpu.cpp).
+TrainResult train_multi_gpu(TuckerModel& model, const CooTensor& train_set, const CooTensor* test_set,
+                            const HyperParams& hyper);
+
 // The cached session of `train` for (test, shape, ranks), created on first use.
 Session& session_for(const CooTensor& train, const CooTensor* test, const Shape& shape, const Ranks& ranks,
                      int device = -1);

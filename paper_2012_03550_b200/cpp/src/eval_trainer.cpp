@@ -151,6 +151,9 @@ void HyperParams::validate() const {
   // because its factor phase reads the dense core; the device path never
   // builds it, so the cap is lifted (deviations).
   if (r_core > SGDT_MAX_RCORE) throw ConfigError("R_core above 32 is not supported by the device kernels");
+  if (devices.size() > 8) throw ConfigError("at most 8 devices (one node)");
+  if (devices.size() > 1 && row_fraction < 1.0)
+    throw ConfigError("row fraction < 1 is not supported by the multi-GPU path");
   for (const std::uint32_t j : ranks)
     if (j > SGDT_MAX_J) throw ConfigError("J_n above 64 is not supported by the device kernels");
   if (!(lr_a > 0.0) || !(lr_b > 0.0)) throw ConfigError("learning rates must be positive");
@@ -191,7 +194,13 @@ std::vector<std::string> HyperParams::describe() const {
           "init-stddev = " + g(init_stddev),
           "resample-core-batch = " + std::string(resample_core_batch ? "true" : "false"),
           "incremental-residual = " + std::string(incremental_residual ? "true" : "false"),
-          "device = " + std::to_string(device)};
+          "device = " + std::to_string(device),
+          "devices = " + [&] {
+            std::string d;
+            for (std::size_t i = 0; i < devices.size(); ++i) d += (i ? "," : "") + std::to_string(devices[i]);
+            return d;
+          }(),
+          "core-sharded = " + std::string(core_sharded ? "true" : "false")};
 }
 
 TrainResult train(TuckerModel& model, const CooTensor& train_set, const CooTensor* test_set, const HyperParams& hyper,
@@ -207,6 +216,7 @@ TrainResult train(TuckerModel& model, const CooTensor& train_set, const CooTenso
         throw DomainError("rmse_mae: data exceeds the model's shape in mode " + std::to_string(n + 1));
   }
 
+  if (hyper.devices.size() > 1) return detail::train_multi_gpu(model, train_set, test_set, hyper);
   detail::Session& s = detail::session_for(train_set, test_set, model.shape(), model.ranks(), hyper.device);
   s.sync_model(model);
   Rng rng(hyper.seed + 1);  // batch stream, trainer.cpp:72

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "sgdt_internal.cuh"
+#include "sgdt_qrows.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -90,88 +91,6 @@ __device__ __forceinline__ void column_pass(const float* la, const float* lc, fl
     const float t = lc[rcn * cap + ls] * (xh - lx[ls]);
 #pragma unroll
     for (int q = 0; q < 32; ++q) v[q] = fmaf(t, av[q], v[q]);
-  }
-}
-
-// Q^(k) rows = A^(k) rows x B^(k), a warp per tile of 32 rows: the tile of A
-// (contiguous, row stride J) is staged through a per-warp shared buffer so
-// both the A reads and the Q writes are coalesced; lane l then forms row
-// i0 + l in registers (j ascending, the same fmaf order as a per-row loop).
-constexpr int kQStage = 32 * 33;  // floats per warp
-
-template <int RP>
-__device__ __forceinline__ void q_rows_tiled(const float* __restrict__ A, float* __restrict__ Q, uint32_t J,
-                                             const float* bsk, uint64_t nrows, uint64_t gw, uint64_t nw,
-                                             float* stage, int lane) {
-  for (uint64_t t = gw; t * 32 < nrows; t += nw) {
-    const uint64_t i0 = t * 32;
-    const uint32_t rows = nrows - i0 < 32 ? static_cast<uint32_t>(nrows - i0) : 32u;
-    float q[RP];
-#pragma unroll
-    for (int r = 0; r < RP; ++r) q[r] = 0.f;
-    for (uint32_t j0 = 0; j0 < J; j0 += 32) {
-      const uint32_t jc = J - j0 < 32 ? J - j0 : 32u;
-      __syncwarp();
-      if (jc == J && rows == 32 && (J & 3) == 0) {
-        // full tile, J <= 32: 8 J float4 loads in flight per warp, then scatter
-        const float4* src4 = reinterpret_cast<const float4*>(A + i0 * J);
-        const uint32_t n4 = 8 * J;
-        float4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = u * 32 + lane;
-          v[u] = x < n4 ? __ldg(src4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = u * 32 + lane;
-          if (x < n4) {
-            const uint32_t g = x * 4, row = g / J;
-            float* d = stage + row * 33 + (g - row * J);
-            d[0] = v[u].x;
-            d[1] = v[u].y;
-            d[2] = v[u].z;
-            d[3] = v[u].w;
-          }
-        }
-      } else if (jc == J) {
-        const float* src = A + i0 * J;  // the whole tile is contiguous
-        for (uint32_t g = lane; g < rows * jc; g += 32) {
-          const uint32_t row = g / jc;
-          stage[row * 33 + (g - row * jc)] = __ldg(src + g);
-        }
-      } else {
-        for (uint32_t g = lane; g < rows * jc; g += 32) {
-          const uint32_t row = g / jc, col = g - row * jc;
-          stage[row * 33 + col] = __ldg(A + (i0 + row) * J + j0 + col);
-        }
-      }
-      __syncwarp();
-      if (static_cast<uint32_t>(lane) < rows)
-        for (uint32_t c = 0; c < jc; ++c) {
-          const float av = stage[lane * 33 + c];
-          const float4* br = reinterpret_cast<const float4*>(bsk + (j0 + c) * RP);  // RP % 4 == 0
-#pragma unroll
-          for (int r = 0; r < RP; r += 4) {
-            const float4 b = br[r / 4];
-            q[r] = fmaf(av, b.x, q[r]);
-            q[r + 1] = fmaf(av, b.y, q[r + 1]);
-            q[r + 2] = fmaf(av, b.z, q[r + 2]);
-            q[r + 3] = fmaf(av, b.w, q[r + 3]);
-          }
-        }
-    }
-    __syncwarp();
-    if (static_cast<uint32_t>(lane) < rows) {
-#pragma unroll
-      for (int r = 0; r < RP; ++r) stage[lane * (RP + 1) + r] = q[r];
-    }
-    __syncwarp();
-    float* dst = Q + i0 * RP;
-    for (uint32_t g = lane; g < rows * RP; g += 32) {
-      const uint32_t row = g / RP;
-      dst[g] = stage[row * (RP + 1) + (g - row * RP)];
-    }
   }
 }
 

@@ -125,12 +125,28 @@ struct Params {
   float* Q[kMaxOrder];
 };
 
+// One blocked core phase (sgdt_core_blocked.cu): Psi, the rank's slice of
+// it, the column-block width and the launch geometry of its steps.
+struct CorePlan {
+  bool valid = false;
+  const uint32_t* batch = nullptr;
+  int per_mode = 0;
+  uint64_t m = 0, lo = 0, hi = 0;
+  int world = 1, rank = 0;  // exchange group: the session's ranks (sharded) or itself
+  double lr = 0.0, reg = 0.0;
+  uint32_t T = 1, steps = 0, kstride = 0, js4 = 0, st = 0;
+  int grid = 0;
+  size_t smem = 0;
+  uint32_t next = 0;  // next step to launch (sgdt_core_step checks the order)
+};
+
 struct Session {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // sampler run-ahead (Psi does not depend on the model)
   cudaEvent_t ev_start = nullptr, ev_core = nullptr, ev_samp = nullptr;
+  cudaEvent_t ev_bar = nullptr;  // sgdt_stream_barrier
   int order = 0;
   int rank = 0, world = 1;  // sharded factor phase (multi-GPU)
   uint32_t dims[kMaxOrder] = {};
@@ -198,6 +214,17 @@ struct Session {
   uint64_t cs_cap = 0;
   int core_grid = 0, core_block = 0;
 
+  // blocked / sharded core phase (sgdt_core_blocked.cu)
+  int core_mode = 0;               // 0: cooperative column kernel, 1: blocked steps (single GPU)
+  CorePlan cplan;
+  double* core_x = nullptr;        // exchange buffer: 2 slots x world x core_x_stride fp64 (peer-visible)
+  uint32_t core_x_stride = 0;
+  double* core_peer_x[kMaxPeers + 1] = {};  // every rank's exchange buffer, by rank (sgdt_set_peers)
+  double* core_part = nullptr;     // num_sms x core_x_stride: per-CTA vectors
+  unsigned* core_ticket = nullptr;
+  float *cb_a = nullptr, *cb_c = nullptr, *cb_xh = nullptr, *cb_x = nullptr;  // per-sample state (T < R)
+  uint64_t cb_cap = 0;
+
   // eval
   double* ev_part = nullptr;
   double* ev_out = nullptr;
@@ -240,6 +267,11 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st)
 int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, uint64_t m,
                 int per_mode_batches);
 int launch_q_refresh(Session& s, int mode);
+uint32_t core_block_width(const Session& s, uint64_t m_local, int grid, double step_us, uint32_t requested);
+uint32_t core_block_kstride(const Session& s, uint32_t T);
+uint32_t core_block_max_kstride(const Session& s);
+int plan_core_geometry(Session& s, CorePlan& pl);
+int launch_core_block_step(Session& s, uint32_t k);
 int launch_factor_mode(Session& s, int n, const sgdt_factor_hyper& h, bool subset = false);
 int launch_row_subsets(Session& s, int n, RowSubset& rs, cudaStream_t st);
 int launch_factor_finish(Session& s, int n, const sgdt_factor_hyper& h, uint32_t k, const uint32_t* rows_dev,

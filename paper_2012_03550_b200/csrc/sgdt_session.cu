@@ -642,6 +642,13 @@ void free_session(sgdt_session* s) {
   F(s->cs_xhat);
   F(s->cs_x);
   F(s->cs_part);
+  F(s->core_x);
+  F(s->core_part);
+  F(s->core_ticket);
+  F(s->cb_a);
+  F(s->cb_c);
+  F(s->cb_xh);
+  F(s->cb_x);
   F(s->ev_part);
   F(s->ev_out);
   F(s->flag);
@@ -651,7 +658,7 @@ void free_session(sgdt_session* s) {
   if (s->h_flag) cudaFreeHost(s->h_flag);
   for (auto& e : s->ev)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {s->ev_start, s->ev_core, s->ev_samp})
+  for (cudaEvent_t e : {s->ev_start, s->ev_core, s->ev_samp, s->ev_bar})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev) cudaEventDestroy(e);
   for (cudaEvent_t e : s->ev_copy)
@@ -738,6 +745,50 @@ int enqueue_sample(Session& s, const sgdt_core_hyper& h, uint64_t m, uint32_t* b
   return SGDT_OK;
 }
 
+// Set up a blocked core phase over an already drawn Psi: the slice of it this
+// rank reduces (sharded: partition_even(m, world)[rank], the reference's
+// worker slices, scheduler.cpp:34-46; else all of it), the column-block
+// width and the launch geometry (sgdt_core_blocked.cu).
+int begin_core_plan(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_t* batch, int per_mode,
+                    bool sharded, uint32_t block) {
+  CorePlan& pl = s.cplan;
+  pl = CorePlan{};
+  pl.batch = batch;
+  pl.per_mode = per_mode;
+  pl.m = m;
+  pl.world = sharded ? s.world : 1;
+  pl.rank = sharded ? s.rank : 0;
+  const uint64_t base = m / pl.world, rem = m % pl.world;
+  pl.lo = pl.rank * base + std::min<uint64_t>(pl.rank, rem);
+  pl.hi = pl.lo + base + (static_cast<uint64_t>(pl.rank) < rem ? 1 : 0);
+  pl.lr = h.lr;
+  pl.reg = h.reg;
+  const uint64_t len = pl.hi - pl.lo;
+  const int grid_est = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>((len + 255) / 256, 1), s.num_sms));
+  pl.T = core_block_width(s, len, grid_est, pl.world > 1 ? 20.0 : 5.0, block);
+  TRY(plan_core_geometry(s, pl));
+  if (pl.T < s.R && len > s.cb_cap) {  // per-sample state kept across the blocks of a mode
+    auto F = [](void* p) {
+      if (p) cudaFree(p);
+    };
+    SGDT_CUDA(cudaStreamSynchronize(s.stream));
+    F(s.cb_a);
+    F(s.cb_c);
+    F(s.cb_xh);
+    F(s.cb_x);
+    s.cb_a = s.cb_c = s.cb_xh = s.cb_x = nullptr;
+    s.cb_cap = 0;
+    TRY(dalloc(&s.cb_a, len * pl.js4));
+    TRY(dalloc(&s.cb_c, len * s.RP));
+    TRY(dalloc(&s.cb_xh, len));
+    TRY(dalloc(&s.cb_x, len));
+    s.cb_cap = len;
+  }
+  pl.valid = true;
+  pl.next = 0;
+  return SGDT_OK;
+}
+
 // Enqueue one core phase (no host sync).  `presampled` != nullptr: Psi was
 // already drawn (run-ahead on the side stream) into that buffer.
 int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_t* presampled = nullptr) {
@@ -758,6 +809,12 @@ int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_
       TRY(enqueue_sample(s, h, m, s.batch, s.stream));
     }
     batch = s.batch;
+  }
+  if (s.core_mode == 1) {  // blocked steps, this rank alone (replicated semantics)
+    TRY(begin_core_plan(s, h, m, batch, per_mode ? 1 : 0, false, 0));
+    for (uint32_t k = 0; k < s.cplan.steps; ++k) TRY(launch_core_block_step(s, k));
+    s.cplan.valid = false;
+    return SGDT_OK;
   }
   return launch_core(s, h, batch, m, per_mode ? 1 : 0);
 }
@@ -1038,7 +1095,7 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     SGDT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SGDT_CUDA(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
     for (auto& e : s->ev) SGDT_CUDA(cudaEventCreate(&e));
-    for (cudaEvent_t* e : {&s->ev_start, &s->ev_core, &s->ev_samp})
+    for (cudaEvent_t* e : {&s->ev_start, &s->ev_core, &s->ev_samp, &s->ev_bar})
       SGDT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     if (const char* cs = std::getenv("SGDT_CHUNK_SIZE")) {
       const long v = std::strtol(cs, nullptr, 10);
@@ -1149,6 +1206,16 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     TRY(dalloc(&s->merge_rows, 2));
     TRY(dalloc(&s->merge_g, 2ull * s->RP));
     TRY(dalloc(&s->d_peers, kMaxOrder));
+    // blocked / sharded core phase: exchange buffer, per-CTA vectors, ticket
+    s->core_x_stride = core_block_max_kstride(*s);
+    TRY(dalloc(&s->core_x, 2ull * world * s->core_x_stride));
+    SGDT_CUDA(cudaMemsetAsync(s->core_x, 0, 2ull * world * s->core_x_stride * sizeof(double), s->stream));
+    // per-CTA vectors, then one slot per 16-CTA reduction group
+    TRY(dalloc(&s->core_part, static_cast<uint64_t>(s->num_sms + s->num_sms / 16 + 1) * s->core_x_stride));
+    TRY(dalloc(&s->core_ticket, 64));  // [0]: groups done, [1 + g]: CTAs of group g done
+    SGDT_CUDA(cudaMemsetAsync(s->core_ticket, 0, 64 * sizeof(unsigned), s->stream));
+    s->core_peer_x[rank] = s->core_x;
+    if (const char* e = std::getenv("SGDT_CORE")) s->core_mode = std::strcmp(e, "blocked") == 0 ? 1 : 0;
     // sampler
     TRY(dalloc(&s->mt, 313));
     uint64_t mt[313];
@@ -1769,16 +1836,17 @@ int sgdt_peer_buffers(sgdt_session* s, void** ptrs) {
     ptrs[s->order + k] = s->P.Q[k];
   }
   ptrs[2 * s->order] = s->xrec;
+  ptrs[2 * s->order + 1] = s->core_x;
   return SGDT_OK;
 }
 
 int sgdt_peer_ipc_handles(sgdt_session* s, void* handles) {
   if (!s || !handles) return fail(SGDT_ERR_DOMAIN, "null argument");
   SGDT_CUDA(cudaSetDevice(s->device));
-  void* ptrs[2 * kMaxOrder + 1];
+  void* ptrs[2 * kMaxOrder + 2];
   TRY(sgdt_peer_buffers(s, ptrs));
   auto* out = static_cast<cudaIpcMemHandle_t*>(handles);
-  for (int i = 0; i < 2 * s->order + 1; ++i) SGDT_CUDA(cudaIpcGetMemHandle(&out[i], ptrs[i]));
+  for (int i = 0; i < 2 * s->order + 2; ++i) SGDT_CUDA(cudaIpcGetMemHandle(&out[i], ptrs[i]));
   return SGDT_OK;
 }
 
@@ -1795,12 +1863,13 @@ int sgdt_set_peers(sgdt_session* s, const void* const* ptrs) {
   if (!s || !ptrs) return fail(SGDT_ERR_DOMAIN, "null argument");
   if (s->world - 1 > kMaxPeers) return fail(SGDT_ERR_CONFIG, "set_peers: at most 8 ranks");
   SGDT_CUDA(cudaSetDevice(s->device));
-  const int per = 2 * s->order + 1;
+  const int per = 2 * s->order + 2;
   PeerTable tab[kMaxOrder] = {};
   int np = 0;
   for (int r = 0; r < s->world; ++r) {
-    if (r == s->rank) continue;
     const void* const* row = ptrs + static_cast<size_t>(r) * per;
+    s->core_peer_x[r] = r == s->rank ? s->core_x : static_cast<double*>(const_cast<void*>(row[2 * s->order + 1]));
+    if (r == s->rank) continue;
     for (int k = 0; k < s->order; ++k) {
       tab[k].A[np] = static_cast<float*>(const_cast<void*>(row[k]));
       tab[k].Q[np] = static_cast<float*>(const_cast<void*>(row[s->order + k]));
@@ -1830,6 +1899,54 @@ int sgdt_core_epoch_async(sgdt_session* s, const sgdt_core_hyper* h) {
   }
   if (h->lr == 0.0) return SGDT_OK;
   return enqueue_core(*s, *h, m);
+}
+
+int sgdt_core_plan(sgdt_session* s, const sgdt_core_hyper* h, uint32_t block, uint32_t* steps, uint32_t* T_out) {
+  if (!s || !steps) return fail(SGDT_ERR_DOMAIN, "null argument");
+  uint64_t m = 0;
+  TRY(check_core_hyper(*s, h, &m));
+  SGDT_CUDA(cudaSetDevice(s->device));
+  *steps = 0;
+  if (T_out) *T_out = 0;
+  const int per_mode = h->resample_per_mode && h->batch_m != 0 ? 1 : 0;
+  const uint32_t* batch = nullptr;
+  if (s->ahead_valid) {
+    if (h->lr == 0.0 || s->ahead_m != m || s->ahead_per_mode != per_mode)
+      return fail(SGDT_ERR_CONFIG, "core_plan: hyper-parameters differ from the pending sgdt_sample_ahead");
+    s->ahead_valid = false;
+    SGDT_CUDA(cudaStreamWaitEvent(s->stream, s->ev_samp, 0));
+    batch = s->batch + static_cast<uint64_t>(s->ahead_slot) * s->order * m;
+  }
+  if (h->lr == 0.0) return SGDT_OK;  // frozen: no steps, no RNG
+  TRY(ensure_batch_capacity(*s, m));
+  s->core_slot = batch && batch != s->batch ? 1 : 0;
+  if (!batch) {
+    if (h->batch_m == 0) {
+      iota32_kernel<<<grid_for(m, s->num_sms), 256, 0, s->stream>>>(s->batch, m);
+      SGDT_CUDA(cudaGetLastError());
+      ++s->launches;
+      s->last_batch = s->batch;
+      s->last_batch_len = m;
+    } else {
+      TRY(enqueue_sample(*s, *h, m, s->batch, s->stream));
+    }
+    batch = s->batch;
+  }
+  TRY(begin_core_plan(*s, *h, m, batch, per_mode, true, block));
+  *steps = s->cplan.steps;
+  if (T_out) *T_out = s->cplan.T;
+  return SGDT_OK;
+}
+
+int sgdt_core_step(sgdt_session* s, uint32_t k) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  CorePlan& pl = s->cplan;
+  if (!pl.valid) return fail(SGDT_ERR_CONFIG, "core_step: no core plan (sgdt_core_plan)");
+  if (k != pl.next) return fail(SGDT_ERR_CONFIG, "core_step: steps must be launched in order");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  TRY(launch_core_block_step(*s, k));
+  if (++pl.next == pl.steps) pl.valid = false;
+  return SGDT_OK;
 }
 
 int sgdt_sample_ahead(sgdt_session* s, const sgdt_core_hyper* h) {
@@ -1893,6 +2010,47 @@ int sgdt_factor_merge_p2p(sgdt_session* s, int mode, const sgdt_factor_hyper* h)
   SGDT_CUDA(cudaGetLastError());
   ++s->launches;
   return launch_factor_finish(*s, mode, *h, k, s->merge_rows, s->merge_g);
+}
+
+int sgdt_enable_peer_access(const int* devices, int n) {
+  if (!devices || n < 1) return fail(SGDT_ERR_DOMAIN, "enable_peer_access: no devices");
+  int cur = 0;
+  SGDT_CUDA(cudaGetDevice(&cur));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      if (devices[i] == devices[j]) continue;
+      int ok = 0;
+      SGDT_CUDA(cudaDeviceCanAccessPeer(&ok, devices[i], devices[j]));
+      if (!ok)
+        return fail(SGDT_ERR_CONFIG, "device " + std::to_string(devices[i]) + " cannot access device " +
+                                         std::to_string(devices[j]) + " (no P2P)");
+      SGDT_CUDA(cudaSetDevice(devices[i]));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        cudaSetDevice(cur);
+        return fail(SGDT_ERR_INTERNAL, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      }
+    }
+  SGDT_CUDA(cudaSetDevice(cur));
+  return SGDT_OK;
+}
+
+int sgdt_stream_barrier(sgdt_session* const* sessions, int n) {
+  if (!sessions || n < 1) return fail(SGDT_ERR_DOMAIN, "stream_barrier: no sessions");
+  for (int i = 0; i < n; ++i) {
+    if (!sessions[i]) return fail(SGDT_ERR_DOMAIN, "stream_barrier: null session");
+    SGDT_CUDA(cudaSetDevice(sessions[i]->device));
+    SGDT_CUDA(cudaEventRecord(sessions[i]->ev_bar, sessions[i]->stream));
+  }
+  for (int i = 0; i < n; ++i) {
+    SGDT_CUDA(cudaSetDevice(sessions[i]->device));
+    for (int j = 0; j < n; ++j)
+      if (j != i) SGDT_CUDA(cudaStreamWaitEvent(sessions[i]->stream, sessions[j]->ev_bar, 0));
+  }
+  return SGDT_OK;
 }
 
 int sgdt_check(sgdt_session* s) {

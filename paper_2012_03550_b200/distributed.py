@@ -1,14 +1,22 @@
 """Multi-GPU SGD_Tucker epochs: the factor phase is sharded over ranks, the
-core phase is replicated.
+core phase is sharded or replicated.
 
 One process (or thread) per GPU, each holding a sharded session
 (`sgdt_session_create_shard`).  Per epoch:
 
-* Core phase, replicated.  Every rank draws the identical Psi (same RNG state,
-  same pool, bit-exact sampler) and runs the identical core kernel on the
-  identical model, so B^(n) stays bit-identical everywhere with no collective.
-  M is small (64-256k samples), so the N x R latency-bound reductions a
-  sharded core phase would need cost more than the replicated compute.
+* Core phase.  Every rank draws the identical Psi (same RNG state, same pool,
+  bit-exact sampler).
+  - sharded (core="sharded", `core_epoch_sharded`): rank r reduces only its
+    slice partition_even(M, P)[r] (the reference's worker slices,
+    scheduler.cpp:34-46).  The columns of B^(n) go in blocks of T; per block
+    each rank stores its B^(n)-gradient vector (V0 and the in-block Gram
+    terms, sgdt.h "sharded core phase") into slot `rank` of every rank's
+    exchange buffer, and after a barrier every rank sums the slots in rank
+    order (core_optimizer.cpp:225-243) and replays the block's Gauss-Seidel
+    column steps, so B^(n) stays bit-identical everywhere.  N ceil(R/T)
+    exchanges per epoch, of ~T^2 J^2 / 2 doubles each.
+  - replicated (core="replicated"): every rank runs the identical core kernel
+    on the identical model; no collective at all.
 * Factor phase, sharded.  For each mode n, in order (Gauss-Seidel):
   1. each rank runs the factor kernel over its slice partition_even(nnz, P)
      of the mode-n order (the `improved` slices of factor_optimizer.cpp:
@@ -179,6 +187,9 @@ def _bind():
     L.sgdt_factor_mode_p2p.argtypes = [vp, C.c_int, C.POINTER(sgdt.FactorHyper)]
     L.sgdt_factor_merge_p2p.argtypes = [vp, C.c_int, C.POINTER(sgdt.FactorHyper)]
     L.sgdt_check.argtypes = [vp]
+    L.sgdt_core_plan.argtypes = [vp, C.POINTER(sgdt.CoreHyper), C.c_uint32, C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_uint32)]
+    L.sgdt_core_step.argtypes = [vp, C.c_uint32]
     L._shard_bound = True
     return L
 
@@ -257,7 +268,7 @@ class ShardedSession(sgdt.Session):
     # ---- peer-memory publication (NVLink P2P) ------------------------------
     @property
     def n_peer_buffers(self) -> int:
-        return 2 * self.order + 1
+        return 2 * self.order + 2
 
     def peer_buffers(self) -> list[int]:
         out = (C.c_void_p * self.n_peer_buffers)()
@@ -270,7 +281,7 @@ class ShardedSession(sgdt.Session):
         return out
 
     def set_peers(self, table) -> None:
-        """table: world x (2N+1) device pointers valid in this process."""
+        """table: world x (2N+2) device pointers valid in this process."""
         flat = [int(p) for row in table for p in row]
         arr = (C.c_void_p * len(flat))(*flat)
         sgdt._ck(_bind().sgdt_set_peers(self.h, arr))
@@ -281,6 +292,15 @@ class ShardedSession(sgdt.Session):
 
     def sample_ahead(self, ch: sgdt.CoreHyper) -> None:
         sgdt._ck(_bind().sgdt_sample_ahead(self.h, C.byref(ch)))
+
+    def core_plan(self, ch: sgdt.CoreHyper, block: int = 0) -> tuple[int, int]:
+        """Begin a sharded core phase; returns (steps, T)."""
+        steps, T = C.c_uint32(), C.c_uint32()
+        sgdt._ck(_bind().sgdt_core_plan(self.h, C.byref(ch), block, C.byref(steps), C.byref(T)))
+        return int(steps.value), int(T.value)
+
+    def core_step(self, k: int) -> None:
+        sgdt._ck(_bind().sgdt_core_step(self.h, k))
 
     def factor_mode_p2p(self, n: int, fh: sgdt.FactorHyper) -> None:
         sgdt._ck(_bind().sgdt_factor_mode_p2p(self.h, n, C.byref(fh)))
@@ -407,13 +427,38 @@ def factor_epoch_p2p(sess, group: Group, fh) -> None:
         group.stream_barrier(sess)
 
 
-def run_epochs_p2p(sess, group: Group, ch, fh, epochs: int = 1) -> None:
-    """`epochs` x (replicated core phase; peer-published sharded factor
-    phase), one host synchronisation (the numeric check) at the end."""
+def core_epoch_sharded(sess, group: Group, ch, block: int = 0) -> int:
+    """update_core_epoch (core_optimizer.cpp:112-257) over P ranks: each rank
+    reduces its Psi slice per column block and publishes the block vector into
+    every rank's exchange slot (P2P stores by the producing kernel); a
+    barrier separates the steps, and the next step sums the slots in rank
+    order.  Backends without peer memory (the CPU stand-in) exchange the
+    vectors through the group instead.  Returns T."""
+    steps, T = sess.core_plan(ch, block)
+    host = getattr(sess, "core_exchange_host", False)
+    for k in range(steps):
+        sess.core_step(k)
+        if k + 1 < steps and group.world > 1:
+            if host:
+                sess.core_receive(group.all_gather(sess.core_vector()))
+            else:
+                group.stream_barrier(sess)
+    return T
+
+
+def run_epochs_p2p(sess, group: Group, ch, fh, epochs: int = 1, core: str = "replicated",
+                   block: int = 0) -> None:
+    """`epochs` x (core phase, replicated or sharded; peer-published sharded
+    factor phase), one host synchronisation (the numeric check) at the end."""
+    if core not in ("replicated", "sharded"):
+        raise ValueError(f"core must be 'replicated' or 'sharded', not {core!r}")
     if not getattr(sess, "peers_set", False):
         connect_peers(sess, group)
     for e in range(epochs):
-        sess.core_epoch_async(ch)
+        if core == "sharded":
+            core_epoch_sharded(sess, group, ch, block)
+        else:
+            sess.core_epoch_async(ch)
         if e + 1 < epochs:  # next epoch's Psi on the side stream, under this factor phase
             sess.sample_ahead(ch)
         factor_epoch_p2p(sess, group, fh)

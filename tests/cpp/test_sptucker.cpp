@@ -409,6 +409,55 @@ void test_resident_per_epoch_calls() {
   or_core_ws_free(&ows);
 }
 
+// Multi-GPU train() (HyperParams::devices; ranks on the same device here:
+// stream-ordered barriers, no kernel waits on another): replicated and
+// sharded core, 2 and 3 ranks, against the single-session train() and the
+// oracle's per-epoch RMSE.
+void test_train_multi_gpu() {
+  const std::vector<std::uint32_t> dims{60, 50, 40};
+  const double sig = unit_sigma(3, 6, 6);
+  const Data d = planted(dims, {6, 6, 6}, 6, 12000, 0.05, 0.0, sig, 3);
+  const CooTensor full = to_tensor(d);
+  auto [tr, te] = train_test_split(full, 0.1, 1);
+  HyperParams h;
+  h.ranks = {6, 6, 6};
+  h.r_core = 6;
+  h.lr_a = h.lr_b = 0.01;
+  h.reg_a = h.reg_b = 0.01;
+  h.batch_m = 1500;
+  h.epochs = 3;
+  h.seed = 2;
+  h.init_mean = 0.0;
+  h.init_stddev = sig;
+  auto [one, r1] = train_from_scratch(tr, &te, h);
+  for (const bool sharded : {false, true})
+    for (const int P : {2, 3}) {
+      HyperParams hm = h;
+      hm.devices.assign(P, 0);
+      hm.core_sharded = sharded;
+      auto [many, rp] = train_from_scratch(tr, &te, hm);
+      CHECK(rp.metrics.size() == r1.metrics.size());
+      for (std::size_t e = 0; e < rp.metrics.size(); ++e) {
+        CHECK(std::abs(rp.metrics[e].train_rmse - r1.metrics[e].train_rmse) <= 1e-4);
+        CHECK(std::abs(rp.metrics[e].test_rmse - r1.metrics[e].test_rmse) <= 1e-4);
+      }
+      double worst = 0.0;
+      for (std::size_t n = 0; n < 3; ++n) {
+        for (std::size_t i = 0; i < many.factor(n).size(); ++i)
+          worst = std::max(worst, std::abs(many.factor(n).data()[i] - one.factor(n).data()[i]) /
+                                      std::max(1.0, std::abs(one.factor(n).data()[i])));
+        for (std::size_t i = 0; i < many.kruskal(n).size(); ++i)
+          worst = std::max(worst, std::abs(many.kruskal(n).data()[i] - one.kruskal(n).data()[i]) /
+                                      std::max(1.0, std::abs(one.kruskal(n).data()[i])));
+      }
+      CHECK(worst <= 1e-4);
+    }
+  HyperParams bad = h;
+  bad.devices = {0, 0};
+  bad.row_fraction = 0.5;
+  CHECK(throws_as<ConfigError>([&] { train_from_scratch(tr, &te, bad); }));
+}
+
 void test_config_errors() {
   const Data d = planted({12, 10, 8}, {3, 3, 3}, 3, 300, 0.02, 0.5, 0.1, 2);
   const CooTensor t = to_tensor(d);
@@ -698,6 +747,7 @@ int main(int argc, char** argv) {
   run("freeze and errors", test_freeze_and_errors);
   run("train end to end", test_train_end_to_end_vs_oracle);
   run("resident per-epoch calls", test_resident_per_epoch_calls);
+  run("multi-GPU train", test_train_multi_gpu);
   run("config errors", test_config_errors);
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -5,6 +5,13 @@ It implements the sharded-session surface that distributed.py drives
 refresh_q) in numpy fp64 with the Kruskal route, so the multi-rank
 orchestration (slices, boundary export, rank-ordered merge, row publication)
 can be exercised under torch.distributed gloo on CPU, where no GPU exists.
+
+It also restates the blocked / sharded core phase (sgdt_core_blocked.cu,
+sgdt.h "sharded core phase") in numpy fp64: Psi from the oracle sampler,
+this rank's partition_even(M, P) slice, per column block the vector of V0
+and the in-block Gram matrices, the rank-ordered sum and the T Gauss-Seidel
+column steps.  Vectors travel through the group (core_exchange_host), since
+there is no peer memory on CPU.
 """
 from __future__ import annotations
 
@@ -115,7 +122,7 @@ class CpuShard:
 
     @property
     def n_peer_buffers(self):
-        return 2 * self.order + 1
+        return 2 * self.order + 2
 
     def peer_buffers(self):
         tok = id(self)
@@ -159,3 +166,71 @@ class CpuShard:
                         g = gg.copy() if g is None else g + gg
             self._finalize(n, row, g, fh)
             self._publish_row(n, row)
+
+    # -- sharded core phase (numpy fp64 restatement of sgdt_core_blocked.cu) --
+    core_exchange_host = True
+
+    def seed(self, seed):
+        from oracle import oracle_py as O
+        self.rng = O.Rng(seed)
+        self.ws = O.CoreWorkspace(len(self.values))
+
+    def core_plan(self, ch, block=0):
+        from oracle import oracle_py as O
+        nnz = len(self.values)
+        m = int(ch.batch_m) or nnz
+        if ch.batch_m:
+            self.psi = O.sample_batch(nnz, m, self.rng, self.ws).astype(np.int64)
+        else:
+            self.psi = np.arange(nnz)
+        self.m = m
+        self.lo, self.hi = partition_even(m, self.world)[self.rank]
+        self.lr, self.reg = float(ch.lr), float(ch.reg)
+        T = min(int(block) if block else self.R, self.R)
+        self.T = T
+        self.blocks = [(n, r0, min(T, self.R - r0)) for n in range(self.order) for r0 in range(0, self.R, T)]
+        self.steps = len(self.blocks) + 1
+        self._vec, self._sum = None, None
+        return self.steps, T
+
+    def _block_vector(self, n, r0, T):
+        ids = self.psi[self.lo:self.hi]
+        co = self.coords[ids]
+        c = np.ones((len(ids), self.R))
+        for k in range(self.order):
+            if k != n:
+                c *= self.A[k][co[:, k]] @ self.B[k]
+        a = self.A[n][co[:, n]]
+        xhat = (c * (a @ self.B[n])).sum(1)
+        res = xhat - self.values[ids]
+        cb = c[:, r0:r0 + T]
+        V0 = np.einsum("st,s,sj->tj", cb, res, a)
+        G = np.einsum("st,su,sj,sk->tujk", cb, cb, a, a)
+        return np.concatenate([V0.ravel(), G.ravel()])
+
+    def _replay(self, n, r0, T, v):
+        J = int(self.J[n])
+        V0 = v[:T * J].reshape(T, J)
+        G = v[T * J:].reshape(T, T, J, J)
+        db = np.zeros((T, J))
+        for t in range(T):
+            V = V0[t] + sum(G[t, u] @ db[u] for u in range(t))
+            old = self.B[n][:, r0 + t].copy()
+            self.B[n][:, r0 + t] = old - self.lr * (V / self.m + self.reg * old)
+            db[t] = self.B[n][:, r0 + t] - old
+
+    def core_step(self, k):
+        if k > 0:
+            v = self._sum if self._sum is not None else self._vec
+            self._replay(*self.blocks[k - 1], v)
+            self._sum = None
+        self._vec = self._block_vector(*self.blocks[k]) if k + 1 < self.steps else None
+
+    def core_vector(self):
+        return self._vec
+
+    def core_receive(self, vecs):
+        acc = np.zeros_like(vecs[0])
+        for v in vecs:  # ascending rank
+            acc = acc + v
+        self._sum = acc

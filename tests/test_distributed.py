@@ -142,6 +142,81 @@ def test_gloo_two_processes(tmp_path):
         assert np.max(np.abs(got - want)) <= 1e-12
 
 
+# ---------------------------------------------------------------- sharded core phase
+class CH:  # CoreHyper look-alike
+    lr, reg, batch_m, resample_per_mode, incremental_residual = 0.02, 0.01, 300, 0, 0
+
+
+def oracle_core(c, v, A, B, seed):
+    m = O.Model(DIMS, J, R)
+    m.set_params(A, B)
+    O.update_core_epoch(m, O.Tensor(DIMS, c, v), CH.lr, CH.reg, CH.batch_m, O.Rng(seed),
+                        O.CoreWorkspace(len(v)))
+    return m.params()[1]
+
+
+def run_core_threads(c, v, A, B, world, block, seed=3):
+    groups = D.ThreadGroup.make(world)
+    sess = [CpuShard(DIMS, c, v, J, R, r, world, A, B) for r in range(world)]
+    errs = []
+
+    def body(r):
+        try:
+            sess[r].seed(seed)
+            D.core_epoch_sharded(sess[r], groups[r], CH, block)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            raise
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    return sess
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 7])
+@pytest.mark.parametrize("block", [1, 2, 3])
+def test_sharded_core_thread_ranks_match_oracle(world, block):
+    """The blocked algebra (V0 + in-block Gram, rank-ordered sums, T exact
+    Gauss-Seidel steps) equals the reference's column-by-column update."""
+    c, v, (A, B) = data(seed=11)
+    want = oracle_core(c, v, A, B, 3)
+    sess = run_core_threads(c, v, A, B, world, block)
+    for s in sess:
+        for n in range(3):
+            assert np.max(np.abs(s.B[n] - want[n])) <= 1e-11
+    for s in sess[1:]:
+        for n in range(3):
+            assert np.array_equal(s.B[n], sess[0].B[n])
+
+
+def _gloo_core_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c, v, (A, B) = data(seed=11)
+    s = CpuShard(DIMS, c, v, J, R, rank, world, A, B)
+    s.seed(3)
+    D.core_epoch_sharded(s, D.TorchGroup(), CH, 2)
+    np.save(os.path.join(out_dir, f"B_{rank}.npy"), np.concatenate([b.ravel() for b in s.B]))
+    dist.destroy_process_group()
+
+
+def test_sharded_core_gloo_two_processes(tmp_path):
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.spawn(_gloo_core_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    c, v, (A, B) = data(seed=11)
+    want = np.concatenate([b.ravel() for b in oracle_core(c, v, A, B, 3)])
+    got = [np.load(tmp_path / f"B_{r}.npy") for r in range(2)]
+    assert np.array_equal(got[0], got[1])
+    assert np.max(np.abs(got[0] - want)) <= 1e-11
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
 def test_gpu_sharded_sessions_match_single_session(world):
