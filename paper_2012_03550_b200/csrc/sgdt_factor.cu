@@ -307,7 +307,27 @@ __device__ __forceinline__ float4 q_ld_r(const float4* p, int j, int r) {
   return q_ld<RP, SJ>(p, j);
 }
 
-template <int RP, int NO, int SJ, bool T2>
+// LM = 2: RP % 8 == 0, each global row is gathered by 256-bit loads
+// (LDG.E.ENL2.256; one load per 32 B instead of two LDG.128).
+__device__ __forceinline__ void ldg256(const float4* p, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+}
+template <int RP, int SJ, int LM>
+__device__ __forceinline__ void q_ld_row(const float4* qk, int j, float4 (&g)[RP / 4]) {
+  if constexpr (LM == 2 && RP % 8 == 0) {
+    if (j != SJ) {
+#pragma unroll
+      for (int r = 0; r < RP / 4; r += 2) ldg256(qk + r, g[r], g[r + 1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RP / 4; ++r) g[r] = q_ld_r<RP, SJ, LM == 1>(qk + r, j, r);
+}
+
+template <int RP, int NO, int SJ, int LM>
 __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn, float* wsc, uint32_t wid,
                                            const float4* qs) {
   const uint32_t lane = threadIdx.x & 31;
@@ -338,9 +358,11 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
 #pragma unroll
         for (int j = 0; j < NO; ++j) {
           const float4* qk = q_row<RP, SJ>(a, j, ld_stream(a.oidx[j] + q), qs);
+          float4 gr[RP / 4];
+          q_ld_row<RP, SJ, LM>(qk, j, gr);
 #pragma unroll
           for (int r = 0; r < RP / 4; ++r) {
-            const float4 t = q_ld_r<RP, SJ, T2>(qk + r, j, r);
+            const float4 t = gr[r];
             c[4 * r] *= t.x;
             c[4 * r + 1] *= t.y;
             c[4 * r + 2] *= t.z;
@@ -406,8 +428,7 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
 #pragma unroll
       for (int j = 0; j < NO; ++j) {
         const float4* qk = q_row<RP, SJ>(a, j, ik[j], qs);
-#pragma unroll
-        for (int r = 0; r < RP / 4; ++r) g[j][r] = q_ld_r<RP, SJ, T2>(qk + r, j, r);
+        q_ld_row<RP, SJ, LM>(qk, j, g[j]);
       }
       const float4* qn = reinterpret_cast<const float4*>(Qn + static_cast<uint64_t>(key) * RP);
       float4 h[RP / 4];
@@ -530,20 +551,20 @@ __device__ __forceinline__ void chunk_body(const FactorArgs& a, const float* bsn
   }
 }
 
-template <int RP, int NO, bool T2>
+template <int RP, int NO, int LM>
 __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   __shared__ __align__(16) float wscr[8 * kWarpScratch];
   load_bsn<RP>(a, bsn);
   __syncthreads();
   const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid < a.n_chunks) chunk_body<RP, NO, -1, T2>(a, bsn, wscr + (threadIdx.x >> 5) * kWarpScratch, wid, nullptr);
+  if (wid < a.n_chunks) chunk_body<RP, NO, -1, LM>(a, bsn, wscr + (threadIdx.x >> 5) * kWarpScratch, wid, nullptr);
 }
 
 // Staged variant: persistent CTAs of kStagedWarps warps copy table SJ into
 // shared memory once, then stride over the chunks.
 constexpr int kStagedWarps = 24;
-template <int RP, int NO, int SJ, bool T2>
+template <int RP, int NO, int SJ, int LM>
 __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   __shared__ __align__(16) float wscr[kStagedWarps * kWarpScratch];
@@ -558,7 +579,7 @@ __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(Fac
   float* wsc = wscr + (threadIdx.x >> 5) * kWarpScratch;
   for (uint32_t wid = blockIdx.x * kStagedWarps + (threadIdx.x >> 5); wid < a.n_chunks;
        wid += gridDim.x * kStagedWarps)
-    chunk_body<RP, NO, SJ, T2>(a, bsn, wsc, wid, qs);
+    chunk_body<RP, NO, SJ, LM>(a, bsn, wsc, wid, qs);
 }
 
 // ---------------------------------------------------------------------------
@@ -876,13 +897,13 @@ int staged_table(const FactorArgs& a) {
   return best;
 }
 
-template <int RP, int NO, int SJ, bool T2>
+template <int RP, int NO, int SJ, int LM>
 cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
   if constexpr (SJ >= NO || RP > 12 || NO > 3) {
     return cudaErrorInvalidValue;
   } else {
     const size_t smem = SJ >= 0 ? static_cast<size_t>(a.orows[SJ < 0 ? 0 : SJ]) * RP * sizeof(float) : 0;
-    auto kern = factor_staged_kernel<RP, NO, SJ, T2>;
+    auto kern = factor_staged_kernel<RP, NO, SJ, LM>;
     // per device (a process may drive several), cheap host calls
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageBytes));
@@ -898,13 +919,13 @@ cudaError_t staged_launch_j(Session& s, const FactorArgs& a) {
   }
 }
 
-template <int RP, int NO, bool T2>
+template <int RP, int NO, int LM>
 cudaError_t staged_launch(Session& s, const FactorArgs& a, int sj) {
   switch (sj) {
-    case -1: return staged_launch_j<RP, NO, -1, T2>(s, a);  // persistent, no staged table
-    case 0: return staged_launch_j<RP, NO, 0, T2>(s, a);
-    case 1: return staged_launch_j<RP, NO, 1, T2>(s, a);
-    case 2: return staged_launch_j<RP, NO, 2, T2>(s, a);
+    case -1: return staged_launch_j<RP, NO, -1, LM>(s, a);  // persistent, no staged table
+    case 0: return staged_launch_j<RP, NO, 0, LM>(s, a);
+    case 1: return staged_launch_j<RP, NO, 1, LM>(s, a);
+    case 2: return staged_launch_j<RP, NO, 2, LM>(s, a);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -928,17 +949,28 @@ int factor_launch(Session& s, FactorArgs& a) {
         return e && atoi(e) == 0;
       }();
       const bool t2 = RP == 12 && a.P.R + 2 <= RP && !t2_off;
+      static const bool w256_off = [] {  // SGDT_LDG256=0: two LDG.128 per 32 B (A/B runs)
+        const char* e = getenv("SGDT_LDG256");
+        return e && atoi(e) == 0;
+      }();
+      const bool w256 = RP % 8 == 0 && !w256_off;
       static const bool persist = [] {  // SGDT_PERSIST=1: persistent launch without a staged table
         const char* e = getenv("SGDT_PERSIST");
         return e && atoi(e) != 0;
       }();
+      constexpr int kLM256 = RP % 8 == 0 ? 2 : 0;
+      constexpr int kLMT2 = RP == 12 ? 1 : 0;
       if (sj >= 0 || (persist && RP <= 12 && NO <= 3)) {
-        const cudaError_t e = t2 ? staged_launch<RP, NO, RP == 12>(s, a, sj) : staged_launch<RP, NO, false>(s, a, sj);
+        const cudaError_t e = t2     ? staged_launch<RP, NO, kLMT2>(s, a, sj)
+                              : w256 ? staged_launch<RP, NO, kLM256>(s, a, sj)
+                                     : staged_launch<RP, NO, 0>(s, a, sj);
         SGDT_CUDA(e);
       } else if (t2) {
-        factor_chunk_kernel<RP, NO, RP == 12><<<grid, block, 0, s.stream>>>(a);
+        factor_chunk_kernel<RP, NO, kLMT2><<<grid, block, 0, s.stream>>>(a);
+      } else if (w256) {
+        factor_chunk_kernel<RP, NO, kLM256><<<grid, block, 0, s.stream>>>(a);
       } else {
-        factor_chunk_kernel<RP, NO, false><<<grid, block, 0, s.stream>>>(a);
+        factor_chunk_kernel<RP, NO, 0><<<grid, block, 0, s.stream>>>(a);
       }
     }
     SGDT_CUDA(cudaGetLastError());
