@@ -175,6 +175,22 @@ int sgdt_factor_epoch_host(sgdt_session* s, const sgdt_factor_hyper* h, double* 
  * host pool gives the new one.  *n = m.  SGDT_ERR_CONFIG when the last call
  * made no or several sampler runs (resample_per_mode): use sgdt_get_pool. */
 int sgdt_pool_delta(sgdt_session* s, uint32_t* pos, uint32_t* val, uint64_t* n);
+/* Record, in every later sampler run, the pool values the run reads (off by
+ * default; the drop-in's per-epoch calls turn it on). */
+int sgdt_set_pool_capture(sgdt_session* s, int on);
+/* sgdt_pool_delta plus the values the run read before it wrote:
+ * pre_j[i] = pool[pos[i]] and pre_lo[i] = pool[i] as they were before the run
+ * (i < m).  A host copy of the pool that agrees with these at every read
+ * position is the pool the device ran on, and after pool[pos[i]] = val[i]
+ * and pool[i] = batch[i] it is the pool the device holds -- every step an
+ * independent per-position check or store (the drop-in does them on host
+ * threads).  SGDT_ERR_CONFIG when capture was off for that run. */
+int sgdt_pool_delta_pre(sgdt_session* s, uint32_t* pos, uint32_t* val, uint32_t* pre_j, uint32_t* pre_lo,
+                        uint64_t* n);
+/* The same four arrays without a copy: pointers into session-owned pinned
+ * host memory, valid until the next sgdt_pool_delta_view / _pre call. */
+int sgdt_pool_delta_view(sgdt_session* s, const uint32_t** pos, const uint32_t** val, const uint32_t** pre_j,
+                         const uint32_t** pre_lo, uint64_t* n);
 /* `epochs` x (core phase; factor phase) enqueued back to back, one host
  * synchronisation at the end (the timed part of train(), trainer.cpp:94-107).
  * A divergence anywhere returns SGDT_ERR_NUMERIC (trainer.cpp:101-103). */

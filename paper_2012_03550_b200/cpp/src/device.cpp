@@ -3,8 +3,11 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <barrier>
 #include <numeric>
 #include <string>
+#include <thread>
 
 namespace sptucker::detail {
 
@@ -109,6 +112,7 @@ sgdt_factor_stats Session::factor_epoch_into(TuckerModel& m, const sgdt_factor_h
 }
 
 void Session::sync_pool(const std::vector<std::uint32_t>& pool, bool force) {
+  check(sgdt_set_pool_capture(h_, 1), "update_core_epoch");
   if (!force && pool.data() == pool_data_ && pool.size() == pool_size_) return;
   check(sgdt_set_pool(h_, pool.data()), "update_core_epoch");
   h2d_bytes += pool.size() * sizeof(std::uint32_t);
@@ -117,16 +121,42 @@ void Session::sync_pool(const std::vector<std::uint32_t>& pool, bool force) {
 }
 
 void Session::pool_reset(const std::vector<std::uint32_t>& iota_pool) {
+  check(sgdt_set_pool_capture(h_, 1), "update_core_epoch");
   check(sgdt_reset_pool(h_), "update_core_epoch");
   pool_data_ = iota_pool.data();
   pool_size_ = iota_pool.size();
 }
 
+namespace {
+// Runs f(thread, lo, hi) over [0, n) on up to 16 host threads; f may call
+// sync() to wait for every thread (a phase barrier).  Random access into the
+// pool is latency bound, so threads pay off long before bandwidth does.
+class Phased {
+ public:
+  explicit Phased(std::size_t n)
+      : n_(n), t_(std::min<std::size_t>({std::max<std::size_t>(1, std::thread::hardware_concurrency()), 16,
+                                         std::max<std::size_t>(1, n / 8192)})),
+        bar_(static_cast<std::ptrdiff_t>(t_)) {}
+  template <class F>
+  void run(F f) {
+    std::vector<std::thread> th;
+    th.reserve(t_ - 1);
+    for (std::size_t k = 1; k < t_; ++k) th.emplace_back([&, k] { f(n_ * k / t_, n_ * (k + 1) / t_); });
+    f(std::size_t{0}, n_ / t_);
+    for (std::thread& x : th) x.join();
+  }
+  void sync() { bar_.arrive_and_wait(); }
+
+ private:
+  std::size_t n_, t_;
+  std::barrier<> bar_;
+};
+}  // namespace
+
 bool Session::pool_apply_checked(std::vector<std::uint32_t>& pool, const std::vector<std::uint32_t>& batch) {
-  const std::size_t m = batch.size();
-  std::vector<std::uint32_t> pos(m), val(m);
   std::uint64_t n = 0;
-  if (sgdt_pool_delta(h_, pos.data(), val.data(), &n) != SGDT_OK) {
+  const std::uint32_t *pos = nullptr, *val = nullptr, *pre_j = nullptr, *pre_lo = nullptr;
+  if (sgdt_pool_delta_view(h_, &pos, &val, &pre_j, &pre_lo, &n) != SGDT_OK) {
     // several runs (resample_per_mode): the pool was uploaded before the
     // call, so the device pool is the truth -- take all of it
     check(sgdt_get_pool(h_, pool.data()), "update_core_epoch");
@@ -135,14 +165,25 @@ bool Session::pool_apply_checked(std::vector<std::uint32_t>& pool, const std::ve
     pool_size_ = pool.size();
     return true;
   }
-  d2h_bytes += 2 * n * sizeof(std::uint32_t);
-  for (std::size_t i = 0; i < n; ++i) std::swap(pool[i], pool[pos[i]]);
-  bool same = std::equal(batch.begin(), batch.end(), pool.begin());
-  for (std::size_t i = 0; same && i < n; ++i) same = pool[pos[i]] == val[i];
-  if (!same) {
-    for (std::size_t i = n; i-- > 0;) std::swap(pool[i], pool[pos[i]]);  // undo
-    return false;
-  }
+  d2h_bytes += 4 * n * sizeof(std::uint32_t);
+  if (n != batch.size()) throw InternalError("pool delta: batch size mismatch");
+  // phase 1: the host pool must hold what the device read at every read
+  // position; phase 2 (only if so): the run's writes -- the touched positions
+  // (a position drawn twice gets the same final value from both draws), then
+  // the batch at 0..m-1
+  std::atomic<bool> same{true};
+  Phased ph(n);
+  ph.run([&](std::size_t lo, std::size_t hi) {
+    bool ok = true;
+    for (std::size_t i = lo; i < hi && ok; ++i) ok = pool[i] == pre_lo[i] && pool[pos[i]] == pre_j[i];
+    if (!ok) same.store(false, std::memory_order_relaxed);
+    ph.sync();
+    if (!same.load(std::memory_order_relaxed)) return;
+    for (std::size_t i = lo; i < hi; ++i) std::atomic_ref<std::uint32_t>(pool[pos[i]]).store(val[i], std::memory_order_relaxed);
+    ph.sync();
+    std::copy(batch.begin() + lo, batch.begin() + hi, pool.begin() + lo);
+  });
+  if (!same.load()) return false;
   pool_data_ = pool.data();
   pool_size_ = pool.size();
   return true;

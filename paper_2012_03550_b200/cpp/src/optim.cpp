@@ -1,7 +1,10 @@
 // optim.cpp -- core and factor phases: the device-backed epoch calls plus the
 // host fp64 per-entry helpers of the reference API.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 
@@ -162,6 +165,24 @@ void grad_a_row_gram(const TuckerModel& model, const CooTensor& t, std::size_t m
 }
 
 // ---------------------------------------------------------------- device epochs
+namespace {
+// SGDT_TRACE_HOST=1: per-call host timing of the per-epoch entry points on
+// stderr (diagnostics of the drop-in's host overhead; off by default).
+struct HostTrace {
+  bool on = [] {
+    const char* e = std::getenv("SGDT_TRACE_HOST");
+    return e && std::atoi(e) != 0;
+  }();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sgdt-host] %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
 CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, const CoreHyper& hyper,
                                  const SchedContext& sched, Rng& rng, CoreBatchWorkspace& ws) {
   if (hyper.lr < 0.0) throw DomainError("core learning rate must be non-negative");
@@ -174,6 +195,7 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
   // changed since this session last synchronised it, the pool only when the
   // host vector is another buffer (device.hpp); several sampler runs per call
   // (resample_per_mode) upload the host pool every time
+  HostTrace tr;
   detail::Session& s = detail::session_for(train, nullptr, model.shape(), model.ranks());
   const bool sampled = hyper.batch_m != 0;
   if (sampled && ws.sample_pool.size() != nnz) {  // sample_batch: a pool of the wrong size restarts from iota
@@ -190,7 +212,9 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
     s.sync_model(model);
     s.put_rng(rng);
     sgdt_core_stats st{};
+    tr.mark("core: sync model/rng/pool");
     detail::check(sgdt_core_epoch(s.get(), &h, &st), "update_core_epoch");
+    tr.mark("core: device epoch");
     if (!sampled) {
       std::iota(ws.batch.begin(), ws.batch.end(), 0u);
       break;
@@ -198,7 +222,10 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
     std::uint64_t len = 0;
     detail::check(sgdt_last_batch(s.get(), ws.batch.data(), &len), "update_core_epoch");
     s.d2h_bytes += m * sizeof(std::uint32_t);
-    if (s.pool_apply_checked(ws.sample_pool, ws.batch)) break;
+    tr.mark("core: batch copy-out");
+    const bool same = s.pool_apply_checked(ws.sample_pool, ws.batch);
+    tr.mark("core: pool delta + host replay check");
+    if (same) break;
     // the host pool was edited at a position this run read: the device ran
     // on a stale pool, so repeat the epoch from the host state (model, RNG
     // and pool are all still the pre-call ones)
@@ -208,6 +235,7 @@ CoreEpochStats update_core_epoch(TuckerModel& model, const CooTensor& train, con
   }
   s.take_model(model, /*factors=*/false, /*kruskal=*/true);  // the core phase wrote B only
   s.take_rng(rng);
+  tr.mark("core: B + rng copy-out");
   std::size_t effective = 0;
   for (const Range& r : partition_even(m, sched.workers()))
     if (!r.empty()) ++effective;
@@ -226,12 +254,15 @@ FactorEpochStats update_factor_epoch(TuckerModel& model, const CooTensor& train,
   for (RowBatchWorkspace& w : per_worker)
     for (std::vector<double>* v : {&w.e, &w.fact1, &w.fact2, &w.grad}) w.grow(*v, jmax);
 
+  HostTrace tr;
   detail::Session& s = detail::session_for(train, nullptr, model.shape(), model.ranks());
   s.sync_model(model);
   s.put_rng(rng);
+  tr.mark("factor: sync model/rng");
   const sgdt_factor_hyper h{hyper.lr, hyper.reg, hyper.row_fraction};
   const sgdt_factor_stats st = s.factor_epoch_into(model, h);  // A^(n) copied out per mode, overlapped
   s.take_rng(rng);
+  tr.mark("factor: device epoch + A copy-out");
 
   FactorEpochStats out;
   out.rows_updated = st.rows_updated;

@@ -191,6 +191,14 @@ struct Session {
   uint32_t* kprev = nullptr;    // m
   uint32_t* lprev = nullptr;    // m
   uint32_t* dval = nullptr;     // m
+  // sgdt_set_pool_capture: the pool values each sampler run reads
+  // (pre_j[i] = pool[j_i], pre_lo[i] = pool[i] before the run), 2 x cap
+  bool capture_pre = false;
+  uint32_t* pool_pre = nullptr;
+  uint64_t pool_pre_cap = 0;
+  uint32_t* d_delta = nullptr;  // 2 x delta_cap (device): draw targets, final values
+  uint32_t* h_delta = nullptr;  // 4 x delta_cap (pinned): sgdt_pool_delta_view
+  uint64_t delta_cap = 0;
   uint32_t* batch = nullptr;    // 2 x order x m: double-buffered Psi (one per mode when resampling)
   uint64_t batch_cap = 0;
   uint64_t last_batch_len = 0;

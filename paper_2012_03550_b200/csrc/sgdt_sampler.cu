@@ -560,6 +560,16 @@ int launch_draws(Session& s, uint64_t m, const DrawPlan& plan, cudaStream_t st) 
   return SGDT_OK;
 }
 
+// The pre-run pool values at the positions a run reads (sgdt_pool_delta_pre).
+__global__ void capture_pre_kernel(uint64_t m, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ draw_j,
+                                   uint32_t* __restrict__ pre_j, uint32_t* __restrict__ pre_lo) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    pre_j[i] = pool[draw_j[i]];
+    pre_lo[i] = pool[i];
+  }
+}
+
 int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st) {
   if (!s.pool_valid) {
     iota_kernel<<<s.num_sms * 4, 256, 0, st>>>(s.pool, s.nnz);
@@ -580,6 +590,17 @@ int launch_sampler(Session& s, uint64_t m, uint32_t* out_batch, cudaStream_t st)
   link_kernel<<<blocks, 256, 0, st>>>(m, s.draw_j, s.head, s.stamp, s.link);
   resolve_kernel<<<blocks, 256, 0, st>>>(m, s.draw_j, nullptr, s.head, s.link, s.stamp, s.kprev, s.lprev);
   chain_kernel<<<blocks, 256, 0, st>>>(m, s.pool, nullptr, s.draw_j, s.kprev, s.lprev, s.dval, out_batch);
+  if (s.capture_pre) {
+    if (m > s.pool_pre_cap) {
+      if (s.pool_pre) SGDT_CUDA(cudaFree(s.pool_pre));
+      s.pool_pre = nullptr;
+      s.pool_pre_cap = 0;
+      SGDT_CUDA(cudaMalloc(&s.pool_pre, 2 * m * sizeof(uint32_t)));
+      s.pool_pre_cap = m;
+    }
+    capture_pre_kernel<<<blocks, 256, 0, st>>>(m, s.pool, s.draw_j, s.pool_pre, s.pool_pre + m);
+    ++s.launches;
+  }
   write_pool_kernel<<<blocks, 256, 0, st>>>(m, s.pool, s.draw_j, s.head, s.link, s.stamp,
                                             out_batch, s.dval);
   SGDT_CUDA(cudaGetLastError());

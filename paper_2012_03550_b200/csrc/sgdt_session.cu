@@ -645,6 +645,9 @@ void free_session(sgdt_session* s) {
   F(s->core_x);
   F(s->core_part);
   F(s->core_ticket);
+  F(s->pool_pre);
+  F(s->d_delta);
+  if (s->h_delta) cudaFreeHost(s->h_delta);
   F(s->cb_a);
   F(s->cb_c);
   F(s->cb_xh);
@@ -1445,6 +1448,59 @@ int sgdt_pool_delta(sgdt_session* s, uint32_t* pos, uint32_t* val, uint64_t* n) 
   cudaFree(d);
   *n = rc == SGDT_OK ? m : 0;
   return rc;
+}
+
+int sgdt_set_pool_capture(sgdt_session* s, int on) {
+  if (!s) return fail(SGDT_ERR_DOMAIN, "null session");
+  s->capture_pre = on != 0;
+  return SGDT_OK;
+}
+
+int sgdt_pool_delta_view(sgdt_session* s, const uint32_t** pos, const uint32_t** val, const uint32_t** pre_j,
+                         const uint32_t** pre_lo, uint64_t* n) {
+  if (!s || !pos || !val || !pre_j || !pre_lo || !n) return fail(SGDT_ERR_DOMAIN, "pool_delta_view: null argument");
+  if (s->ahead_valid || s->sampler_runs != s->delta_base + 1)
+    return fail(SGDT_ERR_CONFIG, "pool_delta: the last call did not make exactly one sampler run");
+  if (!s->capture_pre || !s->pool_pre || s->delta_m > s->pool_pre_cap)
+    return fail(SGDT_ERR_CONFIG, "pool_delta_view: capture is off (sgdt_set_pool_capture)");
+  SGDT_CUDA(cudaSetDevice(s->device));
+  const uint64_t m = s->delta_m;
+  if (m > s->delta_cap) {
+    if (s->d_delta) cudaFree(s->d_delta);
+    if (s->h_delta) cudaFreeHost(s->h_delta);
+    s->d_delta = nullptr;
+    s->h_delta = nullptr;
+    s->delta_cap = 0;
+    TRY(dalloc(&s->d_delta, 2 * m));
+    SGDT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_delta), 4 * m * sizeof(uint32_t), cudaHostAllocDefault));
+    s->delta_cap = m;
+  }
+  pool_delta_kernel<<<grid_for(m, s->num_sms), 256, 0, s->stream>>>(s->draw_j, s->pool, m, s->d_delta,
+                                                                   s->d_delta + m);
+  ++s->launches;
+  SGDT_CUDA(cudaGetLastError());
+  SGDT_CUDA(cudaMemcpyAsync(s->h_delta, s->d_delta, 2 * m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
+  SGDT_CUDA(cudaMemcpyAsync(s->h_delta + 2 * m, s->pool_pre, 2 * m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            s->stream));
+  SGDT_CUDA(cudaStreamSynchronize(s->stream));
+  *pos = s->h_delta;
+  *val = s->h_delta + m;
+  *pre_j = s->h_delta + 2 * m;
+  *pre_lo = s->h_delta + 3 * m;
+  *n = m;
+  return SGDT_OK;
+}
+
+int sgdt_pool_delta_pre(sgdt_session* s, uint32_t* pos, uint32_t* val, uint32_t* pre_j, uint32_t* pre_lo,
+                        uint64_t* n) {
+  if (!pos || !val || !pre_j || !pre_lo || !n) return fail(SGDT_ERR_DOMAIN, "pool_delta_pre: null argument");
+  const uint32_t *p, *v, *a, *b;
+  TRY(sgdt_pool_delta_view(s, &p, &v, &a, &b, n));
+  std::memcpy(pos, p, *n * sizeof(uint32_t));
+  std::memcpy(val, v, *n * sizeof(uint32_t));
+  std::memcpy(pre_j, a, *n * sizeof(uint32_t));
+  std::memcpy(pre_lo, b, *n * sizeof(uint32_t));
+  return SGDT_OK;
 }
 
 int sgdt_factor_epoch_host(sgdt_session* s, const sgdt_factor_hyper* h, double* const* A_out, sgdt_factor_stats* st) {
