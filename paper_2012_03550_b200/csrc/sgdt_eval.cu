@@ -83,6 +83,7 @@ int eval_launch_rp(Session& s, const RecordCopy& rc, int nblocks) {
 }  // namespace
 
 int launch_eval(Session& s, int which, double* rmse, double* mae) {
+  NvtxRange range(which ? "sgdt:eval test" : "sgdt:eval train");
   const RecordCopy& rc = which == 0 ? s.train_rec : s.test_rec;
   if (rc.nnz == 0) return fail(SGDT_ERR_DOMAIN, "rmse_mae: empty entry set");
   uint64_t want = (rc.nnz + kEvalBlock * 8 - 1) / (kEvalBlock * 8);

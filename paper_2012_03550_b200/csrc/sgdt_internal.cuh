@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -255,6 +256,23 @@ struct Session {
   bool timing_valid = false;
   uint64_t launches = 0;  // kernels launched by this session
 };
+
+// NVTX ranges around the enqueue of each phase and mode ("sgdt:core",
+// "sgdt:factor:mode 2", ...): ncu --nvtx --nvtx-include "sgdt:factor:mode 2/"
+// profiles one mode's launches.  Header-only NVTX v3: no-ops unless a tool
+// injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+inline const char* nvtx_mode_name(int n) {
+  static const char* names[kMaxOrder] = {"sgdt:factor:mode 0", "sgdt:factor:mode 1", "sgdt:factor:mode 2",
+                                         "sgdt:factor:mode 3", "sgdt:factor:mode 4", "sgdt:factor:mode 5",
+                                         "sgdt:factor:mode 6", "sgdt:factor:mode 7"};
+  return names[n];
+}
 
 // error plumbing (sgdt_session.cu)
 void set_error(const std::string& msg);

@@ -743,6 +743,7 @@ int check_factor_hyper(const sgdt_factor_hyper* h) {
 
 // Draw the Psi of one epoch (one per mode when resampling) into `buf`.
 int enqueue_sample(Session& s, const sgdt_core_hyper& h, uint64_t m, uint32_t* buf, cudaStream_t st) {
+  NvtxRange range("sgdt:sample");
   const int draws = (h.resample_per_mode && h.batch_m != 0) ? s.order : 1;
   for (int n = 0; n < draws; ++n) TRY(launch_sampler(s, m, buf + static_cast<uint64_t>(n) * m, st));
   return SGDT_OK;
@@ -796,6 +797,7 @@ int begin_core_plan(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint
 // already drawn (run-ahead on the side stream) into that buffer.
 int enqueue_core(Session& s, const sgdt_core_hyper& h, uint64_t m, const uint32_t* presampled = nullptr) {
   if (h.lr == 0.0) return SGDT_OK;  // frozen phase: bit-exact no-op, no RNG
+  NvtxRange range("sgdt:core");
   TRY(ensure_batch_capacity(s, m));
   TRY(ensure_core_capacity(s, m));
   const bool per_mode = h.resample_per_mode && h.batch_m != 0;
@@ -882,6 +884,7 @@ int enqueue_factor(Session& s, const sgdt_factor_hyper& h, bool time_modes, cuda
   if (subset && s.world > 1)
     return fail(SGDT_ERR_CONFIG, "row_fraction < 1 is not supported by the sharded (multi-GPU) factor phase");
   for (int n = 0; n < s.order; ++n) {
+    NvtxRange range(nvtx_mode_name(n));
     if (time_modes) SGDT_CUDA(cudaEventRecord(s.ev[4 + n], s.stream));
     if (mode_ev) SGDT_CUDA(cudaEventRecord(mode_ev[n], s.stream));
     if (subset) {
@@ -2000,7 +2003,10 @@ int sgdt_core_step(sgdt_session* s, uint32_t k) {
   if (!pl.valid) return fail(SGDT_ERR_CONFIG, "core_step: no core plan (sgdt_core_plan)");
   if (k != pl.next) return fail(SGDT_ERR_CONFIG, "core_step: steps must be launched in order");
   SGDT_CUDA(cudaSetDevice(s->device));
-  TRY(launch_core_block_step(*s, k));
+  {
+    NvtxRange range("sgdt:core step");
+    TRY(launch_core_block_step(*s, k));
+  }
   if (++pl.next == pl.steps) pl.valid = false;
   return SGDT_OK;
 }
