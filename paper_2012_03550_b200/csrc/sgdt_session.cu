@@ -256,14 +256,39 @@ int secondary_mode(const Session& s, int n) {
   return best;
 }
 
+// Sort key of entry perm[q] in the mode-n copy: i_n, then (t >= 0) the
+// tiny-table coordinate i_t, then the secondary coordinate i_m:
+// (i_n << 32) | (i_t * dim_m + i_m).
 __global__ void row_key_kernel(const uint32_t* __restrict__ idx, uint64_t nnz, const uint32_t* __restrict__ perm,
-                               uint64_t len, int n, int m, uint64_t* __restrict__ keys) {
+                               uint64_t len, int n, int m, int t, uint32_t dim_m, uint64_t* __restrict__ keys) {
   for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < len;
        q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t e = perm[q];
-    keys[q] = (static_cast<uint64_t>(idx[static_cast<uint64_t>(n) * nnz + e]) << 32) |
-              (m >= 0 ? idx[static_cast<uint64_t>(m) * nnz + e] : 0u);
+    uint32_t lo = m >= 0 ? idx[static_cast<uint64_t>(m) * nnz + e] : 0u;
+    if (t >= 0) lo += idx[static_cast<uint64_t>(t) * nnz + e] * dim_m;
+    keys[q] = (static_cast<uint64_t>(idx[static_cast<uint64_t>(n) * nnz + e]) << 32) | lo;
   }
+}
+
+// Inside a row, entries are ordered by the coordinate of a tiny other mode
+// (<= kTinyRows rows, e.g. the 50-row fourth mode of BASELINE config 3)
+// before the secondary one, so a warp's lanes share that table's rows
+// (shared-memory broadcasts instead of ~15 bank-conflicted wavefronts per
+// random-row LDS) while long rows keep long runs of the secondary mode.
+// Config 3: modes 0-2 4.36 -> 4.18 ms.  With a 2200-row "tiny" table (config
+// 2) the secondary runs break and it is slower, hence the bound.
+// SGDT_ROW_ORDER=notiny turns it off (A/B runs).
+constexpr uint32_t kTinyRows = 256;
+int tiny_mode(const Session& s, int n, int m) {
+  if (m < 0) return -1;
+  if (const char* e = std::getenv("SGDT_ROW_ORDER"))
+    if (std::strcmp(e, "notiny") == 0) return -1;
+  int best = -1;
+  for (int k = 0; k < s.order; ++k)
+    if (k != n && k != m && (best < 0 || s.dims[k] < s.dims[best])) best = k;
+  if (best < 0 || s.dims[best] > kTinyRows || static_cast<uint64_t>(s.dims[best]) * s.dims[m] >= (1ull << 32))
+    return -1;
+  return best;
 }
 
 __global__ void iota_u32_kernel(uint32_t* p, uint64_t n) {
@@ -485,8 +510,9 @@ int build_mode_order(Session& s, int n, const uint32_t* host_perm, uint32_t* d_p
   do {
     if ((rc = dalloc(&k_in, len)) != SGDT_OK) break;
     if ((rc = dalloc(&d_off, off.size())) != SGDT_OK) break;
-    row_key_kernel<<<grid_for(len, s.num_sms), 256, 0, s.stream>>>(s.train_rec.idx, s.nnz, d_perm, len, n, m,
-                                                                    k_in);
+    const int t = tiny_mode(s, n, m);
+    row_key_kernel<<<grid_for(len, s.num_sms), 256, 0, s.stream>>>(s.train_rec.idx, s.nnz, d_perm, len, n, m, t,
+                                                                    m >= 0 ? s.dims[m] : 0u, k_in);
     if (cudaGetLastError() != cudaSuccess) {
       rc = fail(SGDT_ERR_INTERNAL, "row_key_kernel launch failed");
       break;
