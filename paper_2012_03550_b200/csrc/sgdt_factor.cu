@@ -581,7 +581,10 @@ __global__ void __launch_bounds__(256, factor_min_blocks<RP>()) factor_chunk_ker
 
 // Staged variant: persistent CTAs of kStagedWarps warps copy table SJ into
 // shared memory once, then stride over the chunks.
-constexpr int kStagedWarps = 24;
+#ifndef SGDT_STAGED_WARPS
+#define SGDT_STAGED_WARPS 24
+#endif
+constexpr int kStagedWarps = SGDT_STAGED_WARPS;
 template <int RP, int NO, int SJ, int LM>
 __global__ void __launch_bounds__(kStagedWarps * 32, 1) factor_staged_kernel(FactorArgs a) {
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];

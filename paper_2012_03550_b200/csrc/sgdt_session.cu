@@ -1129,16 +1129,22 @@ int sgdt_session_create_shard(const sgdt_tensor_desc* train, const sgdt_tensor_d
     for (auto& e : s->ev) SGDT_CUDA(cudaEventCreate(&e));
     for (cudaEvent_t* e : {&s->ev_start, &s->ev_core, &s->ev_samp, &s->ev_bar})
       SGDT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    if (const char* cs = std::getenv("SGDT_CHUNK_SIZE")) {
-      const long v = std::strtol(cs, nullptr, 10);
-      if (v >= 1 && v <= (1L << 24)) s->chunk_size = static_cast<uint32_t>(v);
-    }
     s->order = train->order;
     s->nnz = train->nnz;
     s->rank = rank;
     s->world = world;
     s->R = R;
     s->RP = (R + 3) & ~3u;
+    // Factor chunk size: 2048 entries, 4096 for the one-entry-per-lane kernels
+    // (RP <= 12) when every warp gets >= 40 chunks of 2048 (config 3: 450M
+    // entries, 109.8 -> 112.4 G updates/s); longer chunks cost balance on
+    // smaller tensors (config 2: 96.3 -> 93.7) and the wide kernels (config 4
+    // 41.2 -> 34.4, config 5 21.7 -> 20.3).  SGDT_CHUNK_SIZE overrides.
+    if (s->RP <= 12 && s->nnz / world / 2048 >= 40ull * s->num_sms * 24) s->chunk_size = 4096;
+    if (const char* cs = std::getenv("SGDT_CHUNK_SIZE")) {
+      const long v = std::strtol(cs, nullptr, 10);
+      if (v >= 1 && v <= (1L << 24)) s->chunk_size = static_cast<uint32_t>(v);
+    }
     s->P.order = s->order;
     s->P.R = R;
     s->P.RP = s->RP;
