@@ -189,12 +189,16 @@ bool Session::pool_apply_checked(std::vector<std::uint32_t>& pool, const std::ve
   return true;
 }
 
-void Session::put_rng(const Rng& r) { check(sgdt_set_rng(h_, r.state_words().data(), r.state_pos()), "rng"); }
+void Session::put_rng(const Rng& r) {
+  check(sgdt_set_rng(h_, r.state_words().data(), r.state_pos()), "rng");
+  h2d_bytes += Rng::kWords * sizeof(std::uint64_t) + sizeof(std::uint32_t);
+}
 
 void Session::take_rng(Rng& r) {
   std::uint64_t words[Rng::kWords];
   std::uint32_t pos = 0;
   check(sgdt_get_rng(h_, words, &pos), "rng");
+  d2h_bytes += Rng::kWords * sizeof(std::uint64_t) + sizeof(std::uint32_t);
   r.set_state(words, pos);
 }
 
