@@ -14,12 +14,32 @@
 //
 // Each CTA owns the contiguous sample slice partition_even(M, grid)[cta]
 // (scheduler.cpp:34-46).  A step's partial V goes to a double-buffered global
-// array; after grid.sync() every CTA sums the partials in CTA order (fp64) and
-// applies the identical update to its shared-memory copy of B, so all CTAs
-// stay bit-identical without a broadcast.  One grid barrier per (n, r_core).
+// array; column j of V belongs to one reducer warp of the grid (CTA j % grid),
+// which sums the CTA partials in CTA order (fp64), takes the sgd_step on
+// b_{j,rc} and publishes the new value; every CTA then installs the identical
+// column in its shared-memory copy of B.  One exchange per (n, r_core).
+//
+// The exchange carries its own arrival flags: a partial (one double) is stored
+// as two 64-bit words {stamp:32 | half:32} and a new column value as one word
+// {stamp:32 | fp32}, the stamp unique to (launch, step).  A 64-bit store is
+// single-copy atomic, so a reader that sees the stamp has the payload: no fence
+// and no counter.  Measured on the B200 (scripts/microbench/exchange_latency.cu):
+// a store becomes visible to a polling load of another SM after ~1000 cycles, so
+// the two hops cost ~2000 cycles plus the 148-way gather, against ~4800 for
+// grid.sync() followed by the all-read-all of the partials (an all-read-all of
+// stamped partials is one hop but its 148 x 148 polls flood the L2: slower).
+// The cooperative launch is kept because it guarantees that all CTAs are
+// co-resident (the polling loops need that).  Slot reuse is safe with two
+// buffers: a CTA writes step s+2 only after it has taken every column of step
+// s+1, which the reducers published after reading every partial of step s+1,
+// which every CTA stored after taking step s.  With the per-sample state in
+// global memory (large M x J) the passes dominate and grid.sync() is used
+// (launch_core); SGDT_CORE_SYNC=grid|red overrides.  SGDT_CORE_TRACE=1 prints
+// CTA 0's cycle counts at the phase boundaries of the first launches.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "sgdt_internal.cuh"
@@ -44,7 +64,11 @@ struct CoreArgs {
   float* sc;          // m x RP      c_{s,r}
   float* sxh;         // m           xhat_s
   float* sx;          // m           x_s
-  double* part;       // 2 x grid x js
+  ulonglong2* part;   // 2 x js x grid stamped partials
+  unsigned long long* res;  // 2 x js stamped new column values
+  uint32_t stamp0;    // stamps of this launch are stamp0 + step + 1
+  int grid_sync;      // exchange through grid.sync() instead of the stamps (A/B)
+  long long* trace;   // SGDT_CORE_TRACE: clock64() of CTA 0 at the phase boundaries
   double lr, reg;
   int* flag;
   int q_refresh;      // fuse Q = A B for every mode at the end
@@ -52,11 +76,13 @@ struct CoreArgs {
   uint32_t cap;       // samples per CTA slice (upper bound)
 };
 
-// Warp transpose-reduce: afterwards lane l holds the warp-wide sum of v[l]
-// (31 shuffles for 32 values; fixed order, so every run forms the same sums).
-__device__ __forceinline__ float warp_reduce32(float (&v)[32], int lane) {
+// Warp transpose-reduce: afterwards lane l holds the warp-wide sum of v[l % JW]
+// (JW - 1 shuffles for the transposition plus log2(32 / JW) butterflies; fixed
+// order, so every run forms the same sums).
+template <int JW>
+__device__ __forceinline__ float warp_reduce(float (&v)[JW], int lane) {
 #pragma unroll
-  for (int h = 16; h > 0; h >>= 1) {
+  for (int h = JW / 2; h > 0; h >>= 1) {
     const bool up = (lane & h) != 0;
 #pragma unroll
     for (int i = 0; i < h; ++i) {
@@ -65,36 +91,68 @@ __device__ __forceinline__ float warp_reduce32(float (&v)[32], int lane) {
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
     }
   }
+#pragma unroll
+  for (int o = JW; o < 32; o <<= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
   return v[0];
 }
 
-// One pass over the CTA's samples for columns j0..j0+31 of V_rcn:
+__device__ __forceinline__ void st_stamped(ulonglong2* p, double x, uint32_t stamp) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  const unsigned long long hi = static_cast<unsigned long long>(stamp) << 32;
+  const unsigned long long w0 = hi | (b & 0xffffffffull), w1 = hi | (b >> 32);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+
+__device__ __forceinline__ ulonglong2 ld_stamped(const ulonglong2* p) {
+  ulonglong2 w;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w.x), "=l"(w.y) : "l"(p) : "memory");
+  return w;
+}
+
+// One pass over the CTA's samples for columns j0..j0+JW-1 of V_rcn:
 //   (upd >= 0)  xhat_s += c_{s,upd} (a_s . delta_b)    -- column upd was just stepped
 //   v_j += c_{s,rcn} (xhat_s - x_s) a_{s,j}
 // a_s is loaded once into registers and feeds both terms.
+template <int JW>
 __device__ __forceinline__ void column_pass(const float* la, const float* lc, float* lxh, const float* lx,
                                             const float* dbv, uint32_t cap, uint32_t nloc, uint32_t jn,
-                                            int upd, uint32_t rcn, uint32_t j0, float (&v)[32]) {
+                                            int upd, uint32_t rcn, uint32_t j0, float (&v)[JW]) {
   for (uint32_t ls = threadIdx.x; ls < nloc; ls += blockDim.x) {
-    float av[32];
+    float av[JW];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * cap + ls] : 0.f;
+    for (int q = 0; q < JW; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * cap + ls] : 0.f;
     float xh = lxh[ls];
     if (upd >= 0) {
       float d = 0.f;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) d = fmaf(av[q], dbv[q], d);
-      for (uint32_t j = 32; j < jn; ++j) d = fmaf(la[j * cap + ls], dbv[j], d);
+      for (int q = 0; q < JW; ++q) d = fmaf(av[q], dbv[q], d);
+      for (uint32_t j = JW; j < jn; ++j) d = fmaf(la[j * cap + ls], dbv[j], d);
       xh = fmaf(lc[upd * cap + ls], d, xh);
       lxh[ls] = xh;
     }
     const float t = lc[rcn * cap + ls] * (xh - lx[ls]);
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = fmaf(t, av[q], v[q]);
+    for (int q = 0; q < JW; ++q) v[q] = fmaf(t, av[q], v[q]);
+  }
+}
+
+// The CTA's partial of V_rcn, columns j0.. in chunks of JW, into wpart[warp][j].
+template <int JW>
+__device__ __forceinline__ void column_partials(const float* la, const float* lc, float* lxh, const float* lx,
+                                                const float* dbv, uint32_t cap, uint32_t nloc, uint32_t jn,
+                                                int upd, uint32_t rcn, double* wrow, int lane) {
+  for (uint32_t j0 = 0; j0 < jn; j0 += JW) {
+    float v[JW];
+#pragma unroll
+    for (int q = 0; q < JW; ++q) v[q] = 0.f;
+    column_pass<JW>(la, lc, lxh, lx, dbv, cap, nloc, jn, j0 == 0 ? upd : -1, rcn, j0, v);
+    const float w = warp_reduce<JW>(v, lane);
+    if (lane < JW && j0 + lane < jn) wrow[j0 + lane] = static_cast<double>(w);
   }
 }
 
 constexpr int kCoreBlock = 512;
+constexpr int kCoreTraceCap = 1024;
 
 template <int RP>
 __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
@@ -115,6 +173,12 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   const uint32_t dbn = a.js > 32 ? a.js : 32;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int ti = 0;
+#define CORE_TRACE()                                                    \
+  do {                                                                  \
+    if (a.trace && blockIdx.x == 0 && tid == 0 && ti < kCoreTraceCap) a.trace[ti++] = clock64(); \
+  } while (0)
+  CORE_TRACE();
   for (int k = 0; k < a.P.order; ++k)
     for (uint32_t i = tid; i < a.P.J[k] * RP; i += blockDim.x) {
       const uint32_t j = i / RP, r = i % RP;
@@ -155,13 +219,33 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
     // ---- per-sample caches: c_{s,r}, a_s, xhat_s, x_s  (:158-180)
     for (uint32_t ls = tid; ls < nloc; ls += blockDim.x) {
       const uint32_t e = batch[s0 + ls];
+      // narrow rows: all coordinates and the value first (one round trip), then the
+      // rows; with RP > 16 the accumulators leave no registers for that
+      constexpr bool kPre = RP <= 16;
+      uint32_t ik[kMaxOrder];
+      if constexpr (kPre) {
+#pragma unroll
+        for (int k = 0; k < kMaxOrder; ++k)
+          ik[k] = k < a.P.order ? __ldg(a.rec_idx + static_cast<uint64_t>(k) * a.nnz + e) : 0u;
+      }
+      const float xval = __ldg(a.rec_val + e);
       float c[RP];
 #pragma unroll
       for (int r = 0; r < RP; ++r) c[r] = 1.f;
+      uint32_t in_ = 0;
       for (int k = 0; k < a.P.order; ++k) {
-        if (k == n) continue;
-        const uint32_t ik = a.rec_idx[static_cast<uint64_t>(k) * a.nnz + e];
-        const float* arow = a.P.A[k] + static_cast<uint64_t>(ik) * a.P.J[k];
+        uint32_t ikk = 0;
+        if constexpr (kPre) {  // ik[k] without a dynamically indexed (local-memory) array
+#pragma unroll
+          for (int q = 0; q < kMaxOrder; ++q) ikk = q == k ? ik[q] : ikk;
+        } else {
+          ikk = a.rec_idx[static_cast<uint64_t>(k) * a.nnz + e];
+        }
+        if (k == n) {
+          in_ = ikk;
+          continue;
+        }
+        const float* arow = a.P.A[k] + static_cast<uint64_t>(ikk) * a.P.J[k];
         float d[RP];
 #pragma unroll
         for (int r = 0; r < RP; ++r) d[r] = 0.f;
@@ -173,7 +257,6 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
 #pragma unroll
         for (int r = 0; r < RP; ++r) c[r] *= d[r];
       }
-      const uint32_t in_ = a.rec_idx[static_cast<uint64_t>(n) * a.nnz + e];
       const float* arow = a.P.A[n] + static_cast<uint64_t>(in_) * jn;
       float p[RP];
 #pragma unroll
@@ -191,52 +274,97 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
         lc[r * a.cap + ls] = c[r];
       }
       lxh[ls] = xh;
-      lx[ls] = a.rec_val[e];
+      lx[ls] = xval;
     }
     __syncthreads();
+    CORE_TRACE();  // mode setup done
 
     int upd = -1;  // column whose step is still to be folded into xhat
     for (uint32_t rc = 0; rc < a.P.R; ++rc, ++step) {
       // ---- partial V over this CTA's slice: V_j = sum_s c_{s,rc} (xhat_s - x_s) a_{s,j},
       // fused with the xhat refresh for the previous column's step
-      double* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
-      for (uint32_t j0 = 0; j0 < jn; j0 += 32) {
-        float v[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = 0.f;
-        column_pass(la, lc, lxh, lx, dbv, a.cap, nloc, jn, j0 == 0 ? upd : -1, rc, j0, v);
-        const float w = warp_reduce32(v, lane);
-        if (j0 + lane < jn) wpart[warp * a.js + j0 + lane] = static_cast<double>(w);
-      }
+      ulonglong2* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
+      const uint32_t stamp = a.stamp0 + step + 1;
+      if (jn <= 8)
+        column_partials<8>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+      else if (jn <= 16)
+        column_partials<16>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+      else
+        column_partials<32>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+      CORE_TRACE();  // warp partials done (warp 0)
       __syncthreads();
+      CORE_TRACE();  // all warps done
       if (tid < static_cast<int>(jn)) {
         double acc = 0.0;
         for (int w = 0; w < nwarps; ++w) acc += wpart[w * a.js + tid];
-        part[static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x] = acc;  // [j][cta]
+        st_stamped(part + static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x, acc, stamp);  // [j][cta]
       }
-      grid.sync();
-      // ---- every CTA: V_j over the CTA partials (a warp per j, fixed lane
-      // striding + butterfly, so every CTA forms the identical sum), then
-      // sgd_step on column rc
-      for (uint32_t j = warp; j < jn; j += nwarps) {
-        const double* pj = part + static_cast<uint64_t>(j) * gridDim.x;
+      CORE_TRACE();  // partial stored
+      if (a.grid_sync) grid.sync();
+      // ---- reducers: column j of V belongs to one warp of the grid (CTA j % grid).  It
+      // sums the CTA partials in CTA order (fixed lane striding + butterfly), takes the
+      // sgd_step on b_{j,rc} and publishes the new value
+      unsigned long long* res = a.res + static_cast<uint64_t>(step & 1) * a.js;
+      for (uint32_t j = blockIdx.x + warp * gridDim.x; j < jn; j += nwarps * gridDim.x) {
+        const ulonglong2* pj = part + static_cast<uint64_t>(j) * gridDim.x;
         double V = 0.0;
-        for (unsigned b = lane; b < gridDim.x; b += 32) V += __ldcg(pj + b);
+        int rounds = 0;
+        for (unsigned b0 = 0; b0 < gridDim.x; b0 += 160) {
+          // up to five slots per lane in flight; a slot is ready when both of
+          // its words carry this step's stamp
+          ulonglong2 w[5];
+          unsigned pending = 0;
+#pragma unroll
+          for (int q = 0; q < 5; ++q)
+            if (b0 + q * 32 + lane < gridDim.x) pending |= 1u << q;
+          while (pending) {
+            ++rounds;
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+              if (pending & (1u << q)) w[q] = ld_stamped(pj + b0 + q * 32 + lane);
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+              if ((pending & (1u << q)) && static_cast<uint32_t>(w[q].x >> 32) == stamp &&
+                  static_cast<uint32_t>(w[q].y >> 32) == stamp)
+                pending &= ~(1u << q);
+          }
+#pragma unroll
+          for (int q = 0; q < 5; ++q)
+            if (b0 + q * 32 + lane < gridDim.x)
+              V += __longlong_as_double(static_cast<long long>((w[q].y << 32) | (w[q].x & 0xffffffffull)));
+        }
+        if (a.trace && blockIdx.x == 0 && tid == 0 && ti < kCoreTraceCap) {
+          a.trace[kCoreTraceCap + ti] = rounds;
+          a.trace[ti++] = clock64();  // partials polled
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) V += __shfl_xor_sync(0xffffffffu, V, o);
         if (lane == 0) {
-          const float bold = bs_base[bso[n] + j * RP + rc];
-          double w = static_cast<double>(bold);
+          double w = static_cast<double>(bs_base[bso[n] + j * RP + rc]);
           int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
           w -= a.lr * (V * inv_m + a.reg * w);
           const float bnew = static_cast<float>(w);
           bad |= !isfinite(bnew) ? 4 : 0;
-          if (bad && blockIdx.x == 0) atomicOr(a.flag, bad);
-          dbv[j] = bnew - bold;
-          bs_base[bso[n] + j * RP + rc] = bnew;
+          if (bad) atomicOr(a.flag, bad);
+          const unsigned long long word =
+              (static_cast<unsigned long long>(stamp) << 32) | static_cast<unsigned long long>(__float_as_uint(bnew));
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(res + j), "l"(word) : "memory");
         }
       }
+      CORE_TRACE();  // reducer role done
+      // ---- every CTA: take the new column (identical everywhere) and the step delta
+      if (tid < static_cast<int>(jn)) {
+        unsigned long long word;
+        do {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(word) : "l"(res + tid) : "memory");
+        } while (static_cast<uint32_t>(word >> 32) != stamp);
+        const float bnew = __uint_as_float(static_cast<uint32_t>(word));
+        const float bold = bs_base[bso[n] + tid * RP + rc];
+        dbv[tid] = bnew - bold;
+        bs_base[bso[n] + tid * RP + rc] = bnew;
+      }
       __syncthreads();
+      CORE_TRACE();  // column stepped
       upd = static_cast<int>(rc);
     }
   }
@@ -246,12 +374,16 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
     for (int k = 0; k < a.P.order; ++k)
       for (uint32_t i = tid; i < a.P.J[k] * a.P.R; i += blockDim.x)
         a.P.B[k][i] = bs_base[bso[k] + (i / a.P.R) * RP + (i % a.P.R)];
+  CORE_TRACE();
   if (!a.q_refresh) return;
   float* stage = dbv + dbn + warp * kQStage;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * nwarps;
   for (int k = 0; k < a.P.order; ++k)
     q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs_base + bso[k], a.P.dims[k], gw, nw, stage, lane);
+  __syncthreads();
+  CORE_TRACE();
+#undef CORE_TRACE
 }
 
 // Standalone Q refresh (used after set_model and by the factor phase when the
@@ -298,6 +430,12 @@ int core_launch_rp(Session& s, CoreArgs& a) {
   const size_t stage = static_cast<size_t>(block / 32) * kQStage * sizeof(float);  // tail Q refresh
   const size_t tail_local = local > stage ? local : stage;
   a.local = smem + tail_local <= 200 * 1024;
+  // exchange: stamped reducers when the per-sample state is in shared memory (the step
+  // is exchange-bound: config 2 0.186 -> 0.166 ms, config 3 0.381 -> 0.364 ms); with the
+  // state in global memory the passes dominate and grid.sync() measured 1 % faster
+  // (config 5).  SGDT_CORE_SYNC=grid|red overrides.
+  a.grid_sync = !a.local;
+  if (const char* e = std::getenv("SGDT_CORE_SYNC")) a.grid_sync = e[0] == 'g';
   smem += a.local ? tail_local : stage;
   if (smem > 48 * 1024)
     SGDT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -305,10 +443,28 @@ int core_launch_rp(Session& s, CoreArgs& a) {
   SGDT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
   if (per_sm < 1) return fail(SGDT_ERR_INTERNAL, "core kernel does not fit on an SM");
   s.core_grid = grid;
+  static long long* d_trace = nullptr;
+  static int traced = 0;
+  const bool trace = std::getenv("SGDT_CORE_TRACE") && traced < 4;
+  if (trace && !d_trace) SGDT_CUDA(cudaMalloc(&d_trace, 2 * kCoreTraceCap * sizeof(long long)));
+  a.trace = trace ? d_trace : nullptr;
+  if (trace) SGDT_CUDA(cudaMemsetAsync(d_trace, 0, 2 * kCoreTraceCap * sizeof(long long), s.stream));
   void* args[] = {&a};
   SGDT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(block),
                                         args, smem, s.stream));
   ++s.launches;
+  if (trace) {  // diagnostics only: CTA 0's cycle counts between the phase boundaries
+    static long long h[2 * kCoreTraceCap];
+    SGDT_CUDA(cudaStreamSynchronize(s.stream));
+    SGDT_CUDA(cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost));
+    ++traced;
+    std::fprintf(stderr, "core trace (grid %d, cycles since start):", grid);
+    for (int i = 1; i < kCoreTraceCap && h[i]; ++i) {
+      std::fprintf(stderr, " %lld", h[i] - h[0]);
+      if (h[kCoreTraceCap + i]) std::fprintf(stderr, "(r%lld)", h[kCoreTraceCap + i]);
+    }
+    std::fprintf(stderr, "\n");
+  }
   return SGDT_OK;
 }
 
@@ -347,6 +503,18 @@ int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, u
   a.sxh = s.cs_xhat;
   a.sx = s.cs_x;
   a.part = s.cs_part;
+  a.res = reinterpret_cast<unsigned long long*>(s.cs_part + 2ull * s.num_sms * js);
+  {
+    // stamps of this launch: core_stamp + 1 .. core_stamp + order * R; on wrap-around
+    // the slots are cleared so that no stale stamp can match
+    const uint32_t steps = static_cast<uint32_t>(s.order) * s.R;
+    if (s.core_stamp > 0xffffffffu - steps - 1) {
+      SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 2ull * (s.num_sms + 1) * js * sizeof(ulonglong2), s.stream));
+      s.core_stamp = 0;
+    }
+    a.stamp0 = s.core_stamp;
+    s.core_stamp += steps;
+  }
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;

@@ -13,10 +13,29 @@ namespace sgdt {
 // i0 + l in registers (j ascending, the same fmaf order as a per-row loop).
 inline constexpr int kQStage = 32 * 33;  // floats per warp
 
+
 template <int RP>
 __device__ __forceinline__ void q_rows_tiled(const float* __restrict__ A, float* __restrict__ Q, uint32_t J,
                                              const float* bsk, uint64_t nrows, uint64_t gw, uint64_t nw,
                                              float* stage, int lane) {
+  // Full tiles with J <= 32: the 32 J floats of a tile are contiguous and 16-B
+  // aligned (i0 J 4 = 128 t J bytes), read as 8 J float4 (up to 8 per lane).  The
+  // next tile's loads are issued as soon as this tile's registers have been
+  // scattered to the stage, so they are in flight during the FMAs and the store.
+  // (RP <= 16 only: with wider rows the next tile's 32 registers spill; measured
+  // config 3 core 0.372 -> 0.364 ms, config 5 3.63 -> 3.70 ms when it was on for RP = 32)
+  constexpr bool kPipe = RP <= 16;
+  const uint32_t n4 = 8 * J, mJ = (65536u + J - 1) / J;
+  float4 v[8];
+  auto load_tile = [&](uint64_t tt) {
+    const float4* src4 = reinterpret_cast<const float4*>(A + tt * 32 * J);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t x = u * 32 + lane;
+      v[u] = x < n4 ? __ldg(src4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if (kPipe && J <= 32 && gw * 32 + 32 <= nrows) load_tile(gw);
   for (uint64_t t = gw; t * 32 < nrows; t += nw) {
     const uint64_t i0 = t * 32;
     const uint32_t rows = nrows - i0 < 32 ? static_cast<uint32_t>(nrows - i0) : 32u;
@@ -27,18 +46,9 @@ __device__ __forceinline__ void q_rows_tiled(const float* __restrict__ A, float*
       const uint32_t jc = J - j0 < 32 ? J - j0 : 32u;
       __syncwarp();
       if (jc == J && rows == 32) {
-        // full tile, J <= 32: the 32 J floats are contiguous and 16-B aligned
-        // (i0 J 4 = 128 t J bytes): 8 J float4 loads in flight per warp, then
-        // a per-element scatter (row = e / J by a 16-bit reciprocal, exact
-        // for e < 1024 and J <= 32)
-        const float4* src4 = reinterpret_cast<const float4*>(A + i0 * J);
-        const uint32_t n4 = 8 * J, mJ = (65536u + J - 1) / J;
-        float4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = u * 32 + lane;
-          v[u] = x < n4 ? __ldg(src4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        if (!kPipe) load_tile(t);
+        // per-element scatter (row = e / J by a 16-bit reciprocal, exact for
+        // e < 1024 and J <= 32)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t x = u * 32 + lane;
@@ -51,6 +61,7 @@ __device__ __forceinline__ void q_rows_tiled(const float* __restrict__ A, float*
             }
           }
         }
+        if (kPipe && (t + nw) * 32 + 32 <= nrows) load_tile(t + nw);
       } else if (jc == J) {
         const float* src = A + i0 * J;  // the whole tile is contiguous
         for (uint32_t g = lane; g < rows * jc; g += 32) {

@@ -743,7 +743,9 @@ int ensure_core_capacity(Session& s, uint64_t m) {
   TRY(dalloc(&s.cs_c, mm * s.RP));
   TRY(dalloc(&s.cs_xhat, mm));
   TRY(dalloc(&s.cs_x, mm));
-  TRY(dalloc(&s.cs_part, 2ull * s.num_sms * js));
+  TRY(dalloc(&s.cs_part, 2ull * (s.num_sms + 1) * js));  // + the new-column words
+  SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 2ull * (s.num_sms + 1) * js * sizeof(ulonglong2), s.stream));
+  s.core_stamp = 0;
   s.cs_cap = m;
   return SGDT_OK;
 }
