@@ -147,6 +147,18 @@ def build_id():
     return h.hexdigest()[:16]
 
 
+def factor_build_id():
+    """Hash of the sources that shape the factor kernels' memory traffic (the
+    kernels, the shared device helpers and the record layout / chunk schedule in
+    the session): stamps profiles/factor_traffic.json, so a change to another
+    phase (core, sampler, eval) does not make the factor capture stale."""
+    h = hashlib.sha256()
+    for name in ("sgdt_factor.cu", "sgdt_internal.cuh", "sgdt_session.cu"):
+        h.update(name.encode())
+        h.update(open(os.path.join(ROOT, "paper_2012_03550_b200", "csrc", name), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -364,13 +376,13 @@ def cpp_dropin_e2e(cfg, spec, trc, trv, m, warmup, steps):
 def factor_traffic(cfg, mode_ms, peak):
     """ncu DRAM / L2 bytes per factor-mode launch group of THIS build
     (profiles/factor_traffic.json, written by scripts/ncu_factor_traffic.py,
-    stamped with build_id()).  None when the file is for another build."""
+    stamped with factor_build_id()).  None when the file is for another build."""
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "factor_traffic.json")))
     except Exception:
         return None
-    if tj.get("build") != build_id():
-        return {"stale": f"profiles/factor_traffic.json is for build {tj.get('build')}, this is {build_id()}"}
+    if tj.get("build") != factor_build_id():
+        return {"stale": f"profiles/factor_traffic.json is for factor build {tj.get('build')}, this is {factor_build_id()}"}
     c = tj.get(f"config{cfg}")
     if not c:
         return None

@@ -8,7 +8,7 @@ For each BASELINE config it profiles one epoch of `bench.py --config C` with
         --cache-control none --clock-control none -k regex:factor_(chunk|staged|group)_kernel
 (warm L2 between launches, as inside the timed epochs), averages the N mode
 launches of the second epoch and writes profiles/factor_traffic.json stamped
-with bench.build_id(), so the bench reports only traffic measured on the
+with bench.factor_build_id(), so the bench reports only traffic measured on the
 build it runs.  Raw CSVs go to gpurun_out/ncu_traffic_c<C>.csv.
 """
 import csv
@@ -58,9 +58,9 @@ def main(argv):
         tj = json.load(open(path))
     except Exception:
         tj = {}
-    if tj.get("build") != bench.build_id():
+    if tj.get("build") != bench.factor_build_id():
         tj = {}
-    tj["build"] = bench.build_id()
+    tj["build"] = bench.factor_build_id()
     tj["how"] = ("ncu --metrics " + ",".join(METRICS) + " --cache-control none --clock-control none, "
                  "the factor-kernel launches of the second epoch of bench.py --steps 1 --warmup 1, mean per mode")
     for c in cfgs:
