@@ -269,6 +269,11 @@ int sgdt_factor_rows(sgdt_session* s, int mode, uint32_t row_lo, uint32_t row_hi
 int sgdt_factor_device_ptr(sgdt_session* s, int mode, void** ptr);
 /* Q^(mode) = A^(mode) B^(mode) for every row. */
 int sgdt_refresh_q(sgdt_session* s, int mode);
+/* Copy rows [row_lo, row_hi) of the device's Kruskal rows Q^(mode) = A^(mode)
+ * B^(mode) (fp32, R_core per row) to host memory.  Diagnostic: the device
+ * counterpart of the reference's core cache (model.cpp:116-122) has no host
+ * mirror; the tests compare it with A B formed on the host. */
+int sgdt_q_rows(sgdt_session* s, int mode, uint32_t row_lo, uint32_t row_hi, float* buf);
 /* Wait for all work of the session (both of its streams). */
 int sgdt_synchronize(sgdt_session* s);
 

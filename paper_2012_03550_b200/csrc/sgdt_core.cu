@@ -71,9 +71,12 @@ struct CoreArgs {
   long long* trace;   // SGDT_CORE_TRACE: clock64() of CTA 0 at the phase boundaries
   double lr, reg;
   int* flag;
-  int q_refresh;      // fuse Q = A B for every mode at the end
-  int local;          // per-sample state of the CTA's slice lives in shared memory
+  int q_refresh;      // bit k: fuse Q^(k) = A^(k) B^(k) at the end (the other modes go to the tensor-core refresh)
+  int local;          // per-sample state of the CTA's slice: 1 shared memory, 0 global scratch, 2 semi
+                      // (a_s in shared memory / registers, xhat and x in shared memory, c_{s,r} global)
   uint32_t cap;       // samples per CTA slice (upper bound)
+  uint32_t nsm;       // semi: samples whose a_s sit in shared memory (row stride nsm); the samples
+                      // nsm + t, t < blockDim, keep a_s in the registers of thread t
 };
 
 // Warp transpose-reduce: afterwards lane l holds the warp-wide sum of v[l % JW]
@@ -112,49 +115,84 @@ __device__ __forceinline__ ulonglong2 ld_stamped(const ulonglong2* p) {
 // One pass over the CTA's samples for columns j0..j0+JW-1 of V_rcn:
 //   (upd >= 0)  xhat_s += c_{s,upd} (a_s . delta_b)    -- column upd was just stepped
 //   v_j += c_{s,rcn} (xhat_s - x_s) a_{s,j}
-// a_s is loaded once into registers and feeds both terms.
-template <int JW>
-__device__ __forceinline__ void column_pass(const float* la, const float* lc, float* lxh, const float* lx,
-                                            const float* dbv, uint32_t cap, uint32_t nloc, uint32_t jn,
-                                            int upd, uint32_t rcn, uint32_t j0, float (&v)[JW]) {
-  for (uint32_t ls = threadIdx.x; ls < nloc; ls += blockDim.x) {
+// a_s is loaded once into registers and feeds both terms.  la holds the first nla
+// samples (row stride capa); with REG the sample nla + threadIdx.x keeps its a_s in
+// areg (JW = 32 covers the whole row, j0 = 0).
+template <int JW, bool REG>
+__device__ __forceinline__ void column_pass(const float* la, uint32_t capa, uint32_t nla, const float* lc,
+                                            uint32_t capc, float* lxh, const float* lx, const float* dbv,
+                                            uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, uint32_t j0,
+                                            float (&v)[JW], const float (&areg)[32]) {
+  for (uint32_t ls = threadIdx.x; ls < nla; ls += blockDim.x) {
     float av[JW];
 #pragma unroll
-    for (int q = 0; q < JW; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * cap + ls] : 0.f;
+    for (int q = 0; q < JW; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * capa + ls] : 0.f;
     float xh = lxh[ls];
     if (upd >= 0) {
       float d = 0.f;
 #pragma unroll
       for (int q = 0; q < JW; ++q) d = fmaf(av[q], dbv[q], d);
-      for (uint32_t j = JW; j < jn; ++j) d = fmaf(la[j * cap + ls], dbv[j], d);
-      xh = fmaf(lc[upd * cap + ls], d, xh);
+      for (uint32_t j = JW; j < jn; ++j) d = fmaf(la[j * capa + ls], dbv[j], d);
+      xh = fmaf(lc[upd * capc + ls], d, xh);
       lxh[ls] = xh;
     }
-    const float t = lc[rcn * cap + ls] * (xh - lx[ls]);
+    const float t = lc[rcn * capc + ls] * (xh - lx[ls]);
 #pragma unroll
     for (int q = 0; q < JW; ++q) v[q] = fmaf(t, av[q], v[q]);
+  }
+  if constexpr (REG) {
+    static_assert(JW == 32, "register-resident samples take the whole row in one pass");
+    const uint32_t ls = nla + threadIdx.x;
+    if (ls < nloc) {
+      float xh = lxh[ls];
+      if (upd >= 0) {
+        float d = 0.f;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) d = fmaf(areg[q], dbv[q], d);  // areg and dbv are zero past jn
+        xh = fmaf(lc[upd * capc + ls], d, xh);
+        lxh[ls] = xh;
+      }
+      const float t = lc[rcn * capc + ls] * (xh - lx[ls]);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = fmaf(t, areg[q], v[q]);
+    }
   }
 }
 
 // The CTA's partial of V_rcn, columns j0.. in chunks of JW, into wpart[warp][j].
-template <int JW>
-__device__ __forceinline__ void column_partials(const float* la, const float* lc, float* lxh, const float* lx,
-                                                const float* dbv, uint32_t cap, uint32_t nloc, uint32_t jn,
-                                                int upd, uint32_t rcn, double* wrow, int lane) {
+template <int JW, bool REG>
+__device__ __forceinline__ void column_partials(const float* la, uint32_t capa, uint32_t nla, const float* lc,
+                                                uint32_t capc, float* lxh, const float* lx, const float* dbv,
+                                                uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, double* wrow,
+                                                int lane, const float (&areg)[32]) {
   for (uint32_t j0 = 0; j0 < jn; j0 += JW) {
     float v[JW];
 #pragma unroll
     for (int q = 0; q < JW; ++q) v[q] = 0.f;
-    column_pass<JW>(la, lc, lxh, lx, dbv, cap, nloc, jn, j0 == 0 ? upd : -1, rcn, j0, v);
+    column_pass<JW, REG>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, j0 == 0 ? upd : -1, rcn, j0, v, areg);
     const float w = warp_reduce<JW>(v, lane);
     if (lane < JW && j0 + lane < jn) wrow[j0 + lane] = static_cast<double>(w);
+  }
+}
+
+// Values j0 .. j0+7 of a factor row (zeros past J): two 128-bit loads when the row
+// is 16-B aligned (J % 4 == 0), else 8 independent scalar loads.
+__device__ __forceinline__ void load_row8(const float* __restrict__ arow, uint32_t j0, uint32_t J, float (&av)[8]) {
+  if ((J & 3u) == 0) {
+    const float4 lo = __ldg(reinterpret_cast<const float4*>(arow + j0));
+    const float4 hi = j0 + 4 < J ? __ldg(reinterpret_cast<const float4*>(arow + j0 + 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    av[0] = lo.x, av[1] = lo.y, av[2] = lo.z, av[3] = lo.w;
+    av[4] = hi.x, av[5] = hi.y, av[6] = hi.z, av[7] = hi.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) av[q] = j0 + q < J ? __ldg(arow + j0 + q) : 0.f;
   }
 }
 
 constexpr int kCoreBlock = 512;
 constexpr int kCoreTraceCap = 1024;
 
-template <int RP>
+template <int RP, bool REG>
 __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned char smem_raw[];
@@ -196,7 +234,8 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   // per-sample state of this slice (local index ls = s - s0): shared memory
   // when it fits, else the global scratch
   float *la, *lc, *lxh, *lx;
-  if (a.local) {
+  uint32_t capa = a.cap, capc = a.cap, nla = nloc;  // row strides of la / lc, samples held in la
+  if (a.local == 1) {
     la = dbv + dbn;
     lc = la + static_cast<uint64_t>(a.cap) * a.js;
     lxh = lc + static_cast<uint64_t>(a.cap) * RP;
@@ -207,7 +246,19 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
     lc = a.sc + cb * RP;
     lxh = a.sxh + cb;
     lx = a.sx + cb;
+    if (a.local == 2) {  // semi: xhat, x and the first nsm samples' a_s in shared memory
+      lxh = dbv + dbn;
+      lx = lxh + a.cap;
+      la = lx + a.cap;
+      capa = a.nsm;
+      nla = nloc < a.nsm ? nloc : a.nsm;
+    }
   }
+  // the a_s rows of the samples beyond la go through the global scratch once per mode
+  float* ga = a.sa + static_cast<uint64_t>(blockIdx.x) * a.cap * a.js;
+  float areg[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) areg[q] = 0.f;
   // per-sample vectors are stored transposed (la[j*cap + ls], lc[r*cap + ls])
   // so that thread-per-sample passes are coalesced / bank-conflict free
   uint32_t step = 0;
@@ -249,10 +300,17 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
         float d[RP];
 #pragma unroll
         for (int r = 0; r < RP; ++r) d[r] = 0.f;
-        for (uint32_t j = 0; j < a.P.J[k]; ++j) {
-          const float av = arow[j];
+        // the row in groups of 8 values, all 8 loads issued before the FMAs (one
+        // memory round trip per group instead of one per value; j ascending as before)
+        for (uint32_t j0 = 0; j0 < a.P.J[k]; j0 += 8) {
+          float av[8];
+          load_row8(arow, j0, a.P.J[k], av);
 #pragma unroll
-          for (int r = 0; r < RP; ++r) d[r] = fmaf(av, bs_base[bso[k] + j * RP + r], d[r]);
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q < a.P.J[k]) {
+#pragma unroll
+              for (int r = 0; r < RP; ++r) d[r] = fmaf(av[q], bs_base[bso[k] + (j0 + q) * RP + r], d[r]);
+            }
         }
 #pragma unroll
         for (int r = 0; r < RP; ++r) c[r] *= d[r];
@@ -261,22 +319,35 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       float p[RP];
 #pragma unroll
       for (int r = 0; r < RP; ++r) p[r] = 0.f;
-      for (uint32_t j = 0; j < jn; ++j) {
-        const float av = arow[j];
-        la[j * a.cap + ls] = av;
+      for (uint32_t j0 = 0; j0 < jn; j0 += 8) {
+        float av[8];
+        load_row8(arow, j0, jn, av);
 #pragma unroll
-        for (int r = 0; r < RP; ++r) p[r] = fmaf(av, bs_base[bso[n] + j * RP + r], p[r]);
+        for (int q = 0; q < 8; ++q)
+          if (j0 + q < jn) {
+            if (ls < nla)
+              la[(j0 + q) * capa + ls] = av[q];
+            else
+              ga[(j0 + q) * a.cap + ls] = av[q];
+#pragma unroll
+            for (int r = 0; r < RP; ++r) p[r] = fmaf(av[q], bs_base[bso[n] + (j0 + q) * RP + r], p[r]);
+          }
       }
       float xh = 0.f;
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
         xh = fmaf(c[r], p[r], xh);
-        lc[r * a.cap + ls] = c[r];
+        lc[r * capc + ls] = c[r];
       }
       lxh[ls] = xh;
       lx[ls] = xval;
     }
     __syncthreads();
+    if constexpr (REG) {  // thread t takes over the a_s of sample nla + t
+      const uint32_t ls = nla + tid;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) areg[q] = ls < nloc && static_cast<uint32_t>(q) < jn ? ga[q * a.cap + ls] : 0.f;
+    }
     CORE_TRACE();  // mode setup done
 
     int upd = -1;  // column whose step is still to be folded into xhat
@@ -285,12 +356,18 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       // fused with the xhat refresh for the previous column's step
       ulonglong2* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
       const uint32_t stamp = a.stamp0 + step + 1;
-      if (jn <= 8)
-        column_partials<8>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+      if constexpr (REG)
+        column_partials<32, true>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+                                  lane, areg);
+      else if (jn <= 8)
+        column_partials<8, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+                                  lane, areg);
       else if (jn <= 16)
-        column_partials<16>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+        column_partials<16, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+                                   lane, areg);
       else
-        column_partials<32>(la, lc, lxh, lx, dbv, a.cap, nloc, jn, upd, rc, wpart + warp * a.js, lane);
+        column_partials<32, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+                                   lane, areg);
       CORE_TRACE();  // warp partials done (warp 0)
       __syncthreads();
       CORE_TRACE();  // all warps done
@@ -380,7 +457,8 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * nwarps;
   for (int k = 0; k < a.P.order; ++k)
-    q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs_base + bso[k], a.P.dims[k], gw, nw, stage, lane);
+    if (a.q_refresh >> k & 1)
+      q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs_base + bso[k], a.P.dims[k], gw, nw, stage, lane);
   __syncthreads();
   CORE_TRACE();
 #undef CORE_TRACE
@@ -404,45 +482,99 @@ __global__ void __launch_bounds__(256) q_refresh_kernel(Params P, int k) {
                    static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5), stage, lane);
 }
 
+// Launch geometry and where the per-sample state of a CTA's slice lives:
+//   local  everything in shared memory (configs 2, 3);
+//   semi   a_s (J floats per sample, read by every column step) in shared memory, and when that
+//          does not hold the whole slice, the a_s of up to one more sample per thread in registers
+//          (J <= 32, RP >= 16 builds); xhat and x in shared memory; c_{s,r} (two columns read per
+//          step) in the L2-resident global scratch (configs 4, 5: the passes were L2-bandwidth bound
+//          with a_s in global memory, 226 KB per CTA and step at config 5);
+//   global everything in the global scratch.
+// SGDT_CORE_STATE=global|semi|local forces a choice when it fits (A/B).
+struct CoreGeom {
+  int grid;
+  size_t smem;
+  bool reg;
+};
+
 template <int RP>
-int core_launch_rp(Session& s, CoreArgs& a) {
+int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   const int block = kCoreBlock;
   size_t bs_floats = 0;
   for (int k = 0; k < s.order; ++k) bs_floats += s.J[k] * RP;
   size_t smem = ((bs_floats + 1) & ~size_t(1)) * sizeof(float) + (block / 32) * a.js * sizeof(double) +
                 (a.js > 32 ? a.js : 32) * sizeof(float);
-  auto kern = core_kernel<RP>;
-  // one CTA per SM keeps grid.sync cheap; small batches use fewer CTAs
+  // one CTA per SM keeps the exchange cheap; small batches use fewer CTAs
   uint64_t want = (a.m + 127) / 128;
   if (want < 1) want = 1;
   int grid = static_cast<int>(want < static_cast<uint64_t>(s.num_sms) ? want : s.num_sms);
   if (a.q_refresh && grid < s.num_sms) {
     uint64_t rows = 0;
-    for (int k = 0; k < s.order; ++k) rows += s.dims[k];
+    for (int k = 0; k < s.order; ++k)
+      if (a.q_refresh >> k & 1) rows += s.dims[k];
     if (rows > static_cast<uint64_t>(grid) * block * 8) grid = s.num_sms;
   }
   if (const char* e = std::getenv("SGDT_CORE_GRID")) {  // diagnostics (A/B runs)
-    const int g = std::atoi(e);
-    if (g >= 1 && g <= s.num_sms) grid = g;
+    const int gg = std::atoi(e);
+    if (gg >= 1 && gg <= s.num_sms) grid = gg;
   }
   a.cap = static_cast<uint32_t>((a.m + grid - 1) / grid);
+  constexpr size_t kBudget = 200 * 1024;
   const size_t local = static_cast<size_t>(a.cap) * (a.js + RP + 2) * sizeof(float);
   const size_t stage = static_cast<size_t>(block / 32) * kQStage * sizeof(float);  // tail Q refresh
-  const size_t tail_local = local > stage ? local : stage;
-  a.local = smem + tail_local <= 200 * 1024;
-  // exchange: stamped reducers when the per-sample state is in shared memory (the step
-  // is exchange-bound: config 2 0.186 -> 0.166 ms, config 3 0.381 -> 0.364 ms); with the
-  // state in global memory the passes dominate and grid.sync() measured 1 % faster
-  // (config 5).  SGDT_CORE_SYNC=grid|red overrides.
-  a.grid_sync = !a.local;
+  const char* force = std::getenv("SGDT_CORE_STATE");
+  a.local = 0;
+  a.nsm = 0;
+  g.reg = false;
+  size_t state = stage;
+  if (smem + (local > stage ? local : stage) <= kBudget && !(force && (force[0] == 'g' || force[0] == 's'))) {
+    a.local = 1;
+    state = local > stage ? local : stage;
+  } else if (!(force && force[0] == 'g')) {
+    const size_t fixed = smem + 2 * static_cast<size_t>(a.cap) * sizeof(float);
+    if (fixed < kBudget) {
+      uint64_t nsm = (kBudget - fixed) / (a.js * sizeof(float));
+      if (const char* e = std::getenv("SGDT_CORE_NSM")) {  // tests: force register-resident samples
+        const uint64_t lim = std::strtoull(e, nullptr, 10);
+        if (lim >= 1 && lim < nsm) nsm = lim;
+      }
+      if (nsm >= a.cap) {
+        nsm = a.cap;
+      } else if (RP >= 16 && a.js <= 32 && nsm + block >= a.cap) {
+        g.reg = true;
+      } else {
+        nsm = 0;
+      }
+      if (nsm) {
+        a.local = 2;
+        a.nsm = static_cast<uint32_t>(nsm);
+        const size_t semi = (2 * static_cast<size_t>(a.cap) + nsm * a.js) * sizeof(float);
+        state = semi > stage ? semi : stage;
+      }
+    }
+  }
+  // exchange: stamped reducers when the passes run from shared memory (the step is
+  // exchange-bound: config 2 0.186 -> 0.166 ms, config 3 0.381 -> 0.364 ms); with the
+  // state in global memory the passes dominate and grid.sync() measured 1 % faster.
+  // SGDT_CORE_SYNC=grid|red overrides.
+  a.grid_sync = a.local == 0;
   if (const char* e = std::getenv("SGDT_CORE_SYNC")) a.grid_sync = e[0] == 'g';
-  smem += a.local ? tail_local : stage;
+  g.grid = grid;
+  g.smem = smem + state;
+  s.core_grid = grid;
+  return SGDT_OK;
+}
+
+template <int RP, bool REG>
+int core_launch_rp(Session& s, CoreArgs& a, size_t smem) {
+  const int block = kCoreBlock;
+  const int grid = s.core_grid;
+  auto kern = core_kernel<RP, REG>;
   if (smem > 48 * 1024)
     SGDT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   SGDT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
   if (per_sm < 1) return fail(SGDT_ERR_INTERNAL, "core kernel does not fit on an SM");
-  s.core_grid = grid;
   static long long* d_trace = nullptr;
   static int traced = 0;
   const bool trace = std::getenv("SGDT_CORE_TRACE") && traced < 4;
@@ -458,7 +590,8 @@ int core_launch_rp(Session& s, CoreArgs& a) {
     SGDT_CUDA(cudaStreamSynchronize(s.stream));
     SGDT_CUDA(cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost));
     ++traced;
-    std::fprintf(stderr, "core trace (grid %d, cycles since start):", grid);
+    std::fprintf(stderr, "core trace (grid %d, state %d, nsm %u of cap %u, reg %d, sync %s, cycles since start):", grid,
+                 a.local, a.nsm, a.cap, REG ? 1 : 0, a.grid_sync ? "grid" : "stamped");
     for (int i = 1; i < kCoreTraceCap && h[i]; ++i) {
       std::fprintf(stderr, " %lld", h[i] - h[0]);
       if (h[kCoreTraceCap + i]) std::fprintf(stderr, "(r%lld)", h[kCoreTraceCap + i]);
@@ -518,24 +651,45 @@ int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, u
   a.lr = h.lr;
   a.reg = h.reg;
   a.flag = s.flag;
-  a.q_refresh = 1;
-#define CORE_CALL(RP) core_launch_rp<RP>(s, a)
+  // wide modes with many rows are refreshed by the tensor-core kernel after the
+  // cooperative kernel (sgdt_qrefresh_tc.cu); the rest at the kernel's tail
+  int tc_modes = 0;
+  for (int k = 0; k < s.order; ++k)
+    if (q_refresh_tc_eligible(s, k)) tc_modes |= 1 << k;
+  a.q_refresh = ((1 << s.order) - 1) & ~tc_modes;
+  int rc = SGDT_ERR_CONFIG;
+#define CORE_CALL(RP)                                                          \
+  do {                                                                     \
+    CoreGeom g{};                                                          \
+    rc = core_geometry<RP>(s, a, g);                                       \
+    if (rc == SGDT_OK) {                                                   \
+      if constexpr (RP >= 16)                                              \
+        rc = g.reg ? core_launch_rp<RP, true>(s, a, g.smem) : core_launch_rp<RP, false>(s, a, g.smem); \
+      else                                                                 \
+        rc = core_launch_rp<RP, false>(s, a, g.smem);                      \
+    }                                                                      \
+  } while (0)
   switch (s.RP) {
-    case 4: return CORE_CALL(4);
-    case 8: return CORE_CALL(8);
-    case 12: return CORE_CALL(12);
-    case 16: return CORE_CALL(16);
-    case 20: return CORE_CALL(20);
-    case 24: return CORE_CALL(24);
-    case 28: return CORE_CALL(28);
-    case 32: return CORE_CALL(32);
-    default: break;
+    case 4: CORE_CALL(4); break;
+    case 8: CORE_CALL(8); break;
+    case 12: CORE_CALL(12); break;
+    case 16: CORE_CALL(16); break;
+    case 20: CORE_CALL(20); break;
+    case 24: CORE_CALL(24); break;
+    case 28: CORE_CALL(28); break;
+    case 32: CORE_CALL(32); break;
+    default: return fail(SGDT_ERR_CONFIG, "unsupported R_core");
   }
 #undef CORE_CALL
-  return fail(SGDT_ERR_CONFIG, "unsupported R_core");
+  if (rc != SGDT_OK) return rc;
+  for (int k = 0; k < s.order; ++k)
+    if (tc_modes >> k & 1)
+      if (int r2 = launch_q_refresh_tc(s, k)) return r2;
+  return SGDT_OK;
 }
 
 int launch_q_refresh(Session& s, int k) {
+  if (q_refresh_tc_eligible(s, k)) return launch_q_refresh_tc(s, k);
   switch (s.RP) {
     case 4: return q_launch_rp<4>(s, k);
     case 8: return q_launch_rp<8>(s, k);

@@ -7,6 +7,12 @@
 
 namespace sgdt {
 
+// The tensor-core refresh (sgdt_qrefresh_tc.cu: TMA tiles, tcgen05.mma kind::tf32
+// as 3xTF32) serves modes with J = 32, 32-wide Q rows and many rows.
+struct Session;
+bool q_refresh_tc_eligible(const Session& s, int mode);
+int launch_q_refresh_tc(Session& s, int mode);
+
 // Q^(k) rows = A^(k) rows x B^(k), a warp per tile of 32 rows: the tile of A
 // (contiguous, row stride J) is staged through a per-warp shared buffer so
 // both the A reads and the Q writes are coalesced; lane l then forms row

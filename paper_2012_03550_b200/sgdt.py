@@ -281,6 +281,14 @@ class Session:
         _ck(_lib.sgdt_get_model(self.h, pa, pb))
         return A, B
 
+    def q_rows(self, n: int, lo: int = 0, hi: int | None = None) -> np.ndarray:
+        """Rows [lo, hi) of the device's Kruskal rows Q^(n) = A^(n) B^(n) (fp32)."""
+        hi = self.dims[n] if hi is None else hi
+        out = np.empty((hi - lo, self.R), np.float32)
+        _lib.sgdt_q_rows.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_void_p]
+        _ck(_lib.sgdt_q_rows(self.h, n, lo, hi, out.ctypes.data_as(C.c_void_p)))
+        return out
+
     def set_rng(self, state: np.ndarray, pos: int) -> None:
         state = np.ascontiguousarray(state, np.uint64)
         _ck(_lib.sgdt_set_rng(self.h, _p(state, C.c_uint64), pos))
