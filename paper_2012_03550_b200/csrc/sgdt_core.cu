@@ -59,8 +59,9 @@ struct CoreArgs {
   const uint32_t* batch;  // Psi (m) or one Psi per mode (order x m)
   int per_mode;
   uint64_t m;
-  uint32_t js;        // sample row stride of sa (max J)
-  float* sa;          // m x js      a^(n)_{i_n(s)}
+  uint32_t js;        // max J
+  uint32_t ja;        // js rounded up to 4: floats per sample of the a_s caches (float4 groups)
+  float* sa;          // m x ja      a^(n)_{i_n(s)}
   float* sc;          // m x RP      c_{s,r}
   float* sxh;         // m           xhat_s
   float* sx;          // m           x_s
@@ -115,24 +116,44 @@ __device__ __forceinline__ ulonglong2 ld_stamped(const ulonglong2* p) {
 // One pass over the CTA's samples for columns j0..j0+JW-1 of V_rcn:
 //   (upd >= 0)  xhat_s += c_{s,upd} (a_s . delta_b)    -- column upd was just stepped
 //   v_j += c_{s,rcn} (xhat_s - x_s) a_{s,j}
-// a_s is loaded once into registers and feeds both terms.  la holds the first nla
-// samples (row stride capa); with REG the sample nla + threadIdx.x keeps its a_s in
-// areg (JW = 32 covers the whole row, j0 = 0).
+// a_s is loaded once into registers and feeds both terms.  The a_s cache is laid out in
+// float4 groups, la4[g * capa + ls] = a_s[4g .. 4g+3] (zero past J): a thread-per-sample
+// pass is conflict-free, takes J/4 128-bit loads per sample and J/4 row offsets (32-bit
+// loads cost ~600 issue slots per sample at J = 32, mostly address arithmetic: config 5
+// pass measured at 15.7k cycles).  la4 holds the first nla samples; with REG the sample
+// nla + threadIdx.x keeps its a_s in areg (JW = 32 covers the whole row, j0 = 0).
 template <int JW, bool REG>
-__device__ __forceinline__ void column_pass(const float* la, uint32_t capa, uint32_t nla, const float* lc,
+__device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, uint32_t nla, const float* lc,
                                             uint32_t capc, float* lxh, const float* lx, const float* dbv,
                                             uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, uint32_t j0,
                                             float (&v)[JW], const float (&areg)[32]) {
+  const float4* db4 = reinterpret_cast<const float4*>(dbv);
+  const uint32_t jn4 = (jn + 3) >> 2, g0 = j0 >> 2;
   for (uint32_t ls = threadIdx.x; ls < nla; ls += blockDim.x) {
     float av[JW];
 #pragma unroll
-    for (int q = 0; q < JW; ++q) av[q] = j0 + q < jn ? la[(j0 + q) * capa + ls] : 0.f;
+    for (int g = 0; g < JW / 4; ++g) {
+      const float4 t = g0 + g < jn4 ? la4[(g0 + g) * capa + ls] : make_float4(0.f, 0.f, 0.f, 0.f);
+      av[4 * g] = t.x, av[4 * g + 1] = t.y, av[4 * g + 2] = t.z, av[4 * g + 3] = t.w;
+    }
     float xh = lxh[ls];
     if (upd >= 0) {
       float d = 0.f;
 #pragma unroll
-      for (int q = 0; q < JW; ++q) d = fmaf(av[q], dbv[q], d);
-      for (uint32_t j = JW; j < jn; ++j) d = fmaf(la[j * capa + ls], dbv[j], d);
+      for (int g = 0; g < JW / 4; ++g) {  // dbv is zero past jn
+        const float4 b = db4[g];
+        d = fmaf(av[4 * g], b.x, d);
+        d = fmaf(av[4 * g + 1], b.y, d);
+        d = fmaf(av[4 * g + 2], b.z, d);
+        d = fmaf(av[4 * g + 3], b.w, d);
+      }
+      for (uint32_t g = JW / 4; g < jn4; ++g) {
+        const float4 t = la4[g * capa + ls], b = db4[g];
+        d = fmaf(t.x, b.x, d);
+        d = fmaf(t.y, b.y, d);
+        d = fmaf(t.z, b.z, d);
+        d = fmaf(t.w, b.w, d);
+      }
       xh = fmaf(lc[upd * capc + ls], d, xh);
       lxh[ls] = xh;
     }
@@ -148,7 +169,13 @@ __device__ __forceinline__ void column_pass(const float* la, uint32_t capa, uint
       if (upd >= 0) {
         float d = 0.f;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) d = fmaf(areg[q], dbv[q], d);  // areg and dbv are zero past jn
+        for (int g = 0; g < 8; ++g) {  // areg and dbv are zero past jn
+          const float4 b = db4[g];
+          d = fmaf(areg[4 * g], b.x, d);
+          d = fmaf(areg[4 * g + 1], b.y, d);
+          d = fmaf(areg[4 * g + 2], b.z, d);
+          d = fmaf(areg[4 * g + 3], b.w, d);
+        }
         xh = fmaf(lc[upd * capc + ls], d, xh);
         lxh[ls] = xh;
       }
@@ -161,7 +188,7 @@ __device__ __forceinline__ void column_pass(const float* la, uint32_t capa, uint
 
 // The CTA's partial of V_rcn, columns j0.. in chunks of JW, into wpart[warp][j].
 template <int JW, bool REG>
-__device__ __forceinline__ void column_partials(const float* la, uint32_t capa, uint32_t nla, const float* lc,
+__device__ __forceinline__ void column_partials(const float4* la, uint32_t capa, uint32_t nla, const float* lc,
                                                 uint32_t capc, float* lxh, const float* lx, const float* dbv,
                                                 uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, double* wrow,
                                                 int lane, const float (&areg)[32]) {
@@ -206,9 +233,9 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
     off += a.P.J[k] * RP;
   }
   const int nwarps = blockDim.x >> 5;
-  double* wpart = reinterpret_cast<double*>(bs_base + ((off + 1) & ~1u));  // nwarps x js
-  float* dbv = reinterpret_cast<float*>(wpart + nwarps * a.js);           // max(js, 32)
-  const uint32_t dbn = a.js > 32 ? a.js : 32;
+  double* wpart = reinterpret_cast<double*>(bs_base + ((off + 3) & ~3u));  // nwarps x js (16-B aligned)
+  float* dbv = reinterpret_cast<float*>(wpart + ((nwarps * a.js + 1) & ~1u));  // max(ja, 32), 16-B aligned
+  const uint32_t dbn = a.ja > 32 ? a.ja : 32;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int ti = 0;
@@ -233,29 +260,34 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   const double inv_m = 1.0 / static_cast<double>(a.m);
   // per-sample state of this slice (local index ls = s - s0): shared memory
   // when it fits, else the global scratch
-  float *la, *lc, *lxh, *lx;
+  // (cap is a multiple of 4, so every piece below stays 16-B aligned)
+  float4* la;
+  float *lc, *lxh, *lx;
   uint32_t capa = a.cap, capc = a.cap, nla = nloc;  // row strides of la / lc, samples held in la
+  const uint32_t ja4 = a.ja >> 2;
+  // the global scratch slice of this CTA: a_s groups [g * cap + ls]
+  float4* ga = reinterpret_cast<float4*>(a.sa + static_cast<uint64_t>(blockIdx.x) * a.cap * a.ja);
   if (a.local == 1) {
-    la = dbv + dbn;
-    lc = la + static_cast<uint64_t>(a.cap) * a.js;
+    float* base = dbv + dbn;
+    la = reinterpret_cast<float4*>(base);
+    lc = base + static_cast<uint64_t>(a.cap) * a.ja;
     lxh = lc + static_cast<uint64_t>(a.cap) * RP;
     lx = lxh + a.cap;
   } else {
     const uint64_t cb = static_cast<uint64_t>(blockIdx.x) * a.cap;
-    la = a.sa + cb * a.js;
+    la = ga;
     lc = a.sc + cb * RP;
     lxh = a.sxh + cb;
     lx = a.sx + cb;
     if (a.local == 2) {  // semi: xhat, x and the first nsm samples' a_s in shared memory
       lxh = dbv + dbn;
       lx = lxh + a.cap;
-      la = lx + a.cap;
+      la = reinterpret_cast<float4*>(lx + a.cap);
       capa = a.nsm;
       nla = nloc < a.nsm ? nloc : a.nsm;
     }
   }
-  // the a_s rows of the samples beyond la go through the global scratch once per mode
-  float* ga = a.sa + static_cast<uint64_t>(blockIdx.x) * a.cap * a.js;
+  (void)ja4;
   float areg[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) areg[q] = 0.f;
@@ -322,13 +354,15 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       for (uint32_t j0 = 0; j0 < jn; j0 += 8) {
         float av[8];
         load_row8(arow, j0, jn, av);
+        {  // av is zero past jn
+          float4* dst = ls < nla ? la + (j0 >> 2) * capa + ls : ga + (j0 >> 2) * a.cap + ls;
+          const uint32_t dstride = ls < nla ? capa : a.cap;
+          dst[0] = make_float4(av[0], av[1], av[2], av[3]);
+          if (j0 + 4 < jn) dst[dstride] = make_float4(av[4], av[5], av[6], av[7]);
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (j0 + q < jn) {
-            if (ls < nla)
-              la[(j0 + q) * capa + ls] = av[q];
-            else
-              ga[(j0 + q) * a.cap + ls] = av[q];
 #pragma unroll
             for (int r = 0; r < RP; ++r) p[r] = fmaf(av[q], bs_base[bso[n] + (j0 + q) * RP + r], p[r]);
           }
@@ -346,7 +380,11 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
     if constexpr (REG) {  // thread t takes over the a_s of sample nla + t
       const uint32_t ls = nla + tid;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) areg[q] = ls < nloc && static_cast<uint32_t>(q) < jn ? ga[q * a.cap + ls] : 0.f;
+      for (int g = 0; g < 8; ++g) {
+        const float4 t = ls < nloc && static_cast<uint32_t>(4 * g) < jn ? ga[g * a.cap + ls]
+                                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        areg[4 * g] = t.x, areg[4 * g + 1] = t.y, areg[4 * g + 2] = t.z, areg[4 * g + 3] = t.w;
+      }
     }
     CORE_TRACE();  // mode setup done
 
@@ -502,8 +540,9 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   const int block = kCoreBlock;
   size_t bs_floats = 0;
   for (int k = 0; k < s.order; ++k) bs_floats += s.J[k] * RP;
-  size_t smem = ((bs_floats + 1) & ~size_t(1)) * sizeof(float) + (block / 32) * a.js * sizeof(double) +
-                (a.js > 32 ? a.js : 32) * sizeof(float);
+  size_t smem = ((bs_floats + 3) & ~size_t(3)) * sizeof(float) +
+                ((static_cast<size_t>(block / 32) * a.js + 1) & ~size_t(1)) * sizeof(double) +
+                (a.ja > 32 ? a.ja : 32) * sizeof(float);
   // one CTA per SM keeps the exchange cheap; small batches use fewer CTAs
   uint64_t want = (a.m + 127) / 128;
   if (want < 1) want = 1;
@@ -518,9 +557,9 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
     const int gg = std::atoi(e);
     if (gg >= 1 && gg <= s.num_sms) grid = gg;
   }
-  a.cap = static_cast<uint32_t>((a.m + grid - 1) / grid);
+  a.cap = (static_cast<uint32_t>((a.m + grid - 1) / grid) + 3u) & ~3u;  // float4-aligned pieces
   constexpr size_t kBudget = 200 * 1024;
-  const size_t local = static_cast<size_t>(a.cap) * (a.js + RP + 2) * sizeof(float);
+  const size_t local = static_cast<size_t>(a.cap) * (a.ja + RP + 2) * sizeof(float);
   const size_t stage = static_cast<size_t>(block / 32) * kQStage * sizeof(float);  // tail Q refresh
   const char* force = std::getenv("SGDT_CORE_STATE");
   a.local = 0;
@@ -533,10 +572,10 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   } else if (!(force && force[0] == 'g')) {
     const size_t fixed = smem + 2 * static_cast<size_t>(a.cap) * sizeof(float);
     if (fixed < kBudget) {
-      uint64_t nsm = (kBudget - fixed) / (a.js * sizeof(float));
+      uint64_t nsm = ((kBudget - fixed) / (a.ja * sizeof(float))) & ~uint64_t(3);
       if (const char* e = std::getenv("SGDT_CORE_NSM")) {  // tests: force register-resident samples
         const uint64_t lim = std::strtoull(e, nullptr, 10);
-        if (lim >= 1 && lim < nsm) nsm = lim;
+        if (lim >= 1 && lim < nsm) nsm = (lim + 3) & ~uint64_t(3);
       }
       if (nsm >= a.cap) {
         nsm = a.cap;
@@ -548,7 +587,7 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
       if (nsm) {
         a.local = 2;
         a.nsm = static_cast<uint32_t>(nsm);
-        const size_t semi = (2 * static_cast<size_t>(a.cap) + nsm * a.js) * sizeof(float);
+        const size_t semi = (2 * static_cast<size_t>(a.cap) + nsm * a.ja) * sizeof(float);
         state = semi > stage ? semi : stage;
       }
     }
@@ -631,6 +670,7 @@ int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, u
   uint32_t js = 0;
   for (int k = 0; k < s.order; ++k) js = s.J[k] > js ? s.J[k] : js;
   a.js = js;
+  a.ja = (js + 3u) & ~3u;
   a.sa = s.cs_a;
   a.sc = s.cs_c;
   a.sxh = s.cs_xhat;

@@ -738,8 +738,9 @@ int ensure_core_capacity(Session& s, uint64_t m) {
   F(s.cs_part);
   uint32_t js = 0;
   for (int k = 0; k < s.order; ++k) js = std::max(js, s.J[k]);
-  const uint64_t mm = m + s.num_sms;  // per-CTA slices of ceil(m / grid) samples
-  TRY(dalloc(&s.cs_a, mm * js));
+  // per-CTA slices of ceil(m / grid) samples rounded up to 4; a_s in float4 groups
+  const uint64_t mm = m + 4ull * s.num_sms;
+  TRY(dalloc(&s.cs_a, mm * ((js + 3u) & ~3u)));
   TRY(dalloc(&s.cs_c, mm * s.RP));
   TRY(dalloc(&s.cs_xhat, mm));
   TRY(dalloc(&s.cs_x, mm));
