@@ -76,6 +76,7 @@ struct CoreArgs {
   int local;          // per-sample state of the CTA's slice: 1 shared memory, 0 global scratch, 2 semi
                       // (a_s in shared memory / registers, xhat and x in shared memory, c_{s,r} global)
   uint32_t cap;       // samples per CTA slice (upper bound)
+  int ring;           // semi: keep a three-column ring of c in shared memory (SGDT_CORE_RING=0: A/B)
   uint32_t nsm;       // semi: samples whose a_s sit in shared memory (row stride nsm); the samples
                       // nsm + t, t < blockDim, keep a_s in the registers of thread t
 };
@@ -123,10 +124,10 @@ __device__ __forceinline__ ulonglong2 ld_stamped(const ulonglong2* p) {
 // pass measured at 15.7k cycles).  la4 holds the first nla samples; with REG the sample
 // nla + threadIdx.x keeps its a_s in areg (JW = 32 covers the whole row, j0 = 0).
 template <int JW, bool REG>
-__device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, uint32_t nla, const float* lc,
-                                            uint32_t capc, float* lxh, const float* lx, const float* dbv,
-                                            uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, uint32_t j0,
-                                            float (&v)[JW], const float (&areg)[32]) {
+__device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, uint32_t nla, const float* c_rcn,
+                                            const float* c_upd, float* lxh, const float* lx, const float* dbv,
+                                            uint32_t nloc, uint32_t jn, int upd, uint32_t j0, float (&v)[JW],
+                                            const float (&areg)[32]) {
   const float4* db4 = reinterpret_cast<const float4*>(dbv);
   const uint32_t jn4 = (jn + 3) >> 2, g0 = j0 >> 2;
   for (uint32_t ls = threadIdx.x; ls < nla; ls += blockDim.x) {
@@ -154,10 +155,10 @@ __device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, ui
         d = fmaf(t.z, b.z, d);
         d = fmaf(t.w, b.w, d);
       }
-      xh = fmaf(lc[upd * capc + ls], d, xh);
+      xh = fmaf(c_upd[ls], d, xh);
       lxh[ls] = xh;
     }
-    const float t = lc[rcn * capc + ls] * (xh - lx[ls]);
+    const float t = c_rcn[ls] * (xh - lx[ls]);
 #pragma unroll
     for (int q = 0; q < JW; ++q) v[q] = fmaf(t, av[q], v[q]);
   }
@@ -176,10 +177,10 @@ __device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, ui
           d = fmaf(areg[4 * g + 2], b.z, d);
           d = fmaf(areg[4 * g + 3], b.w, d);
         }
-        xh = fmaf(lc[upd * capc + ls], d, xh);
+        xh = fmaf(c_upd[ls], d, xh);
         lxh[ls] = xh;
       }
-      const float t = lc[rcn * capc + ls] * (xh - lx[ls]);
+      const float t = c_rcn[ls] * (xh - lx[ls]);
 #pragma unroll
       for (int q = 0; q < 32; ++q) v[q] = fmaf(t, areg[q], v[q]);
     }
@@ -188,15 +189,15 @@ __device__ __forceinline__ void column_pass(const float4* la4, uint32_t capa, ui
 
 // The CTA's partial of V_rcn, columns j0.. in chunks of JW, into wpart[warp][j].
 template <int JW, bool REG>
-__device__ __forceinline__ void column_partials(const float4* la, uint32_t capa, uint32_t nla, const float* lc,
-                                                uint32_t capc, float* lxh, const float* lx, const float* dbv,
-                                                uint32_t nloc, uint32_t jn, int upd, uint32_t rcn, double* wrow,
-                                                int lane, const float (&areg)[32]) {
+__device__ __forceinline__ void column_partials(const float4* la, uint32_t capa, uint32_t nla, const float* c_rcn,
+                                                const float* c_upd, float* lxh, const float* lx, const float* dbv,
+                                                uint32_t nloc, uint32_t jn, int upd, double* wrow, int lane,
+                                                const float (&areg)[32]) {
   for (uint32_t j0 = 0; j0 < jn; j0 += JW) {
     float v[JW];
 #pragma unroll
     for (int q = 0; q < JW; ++q) v[q] = 0.f;
-    column_pass<JW, REG>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, j0 == 0 ? upd : -1, rcn, j0, v, areg);
+    column_pass<JW, REG>(la, capa, nla, c_rcn, c_upd, lxh, lx, dbv, nloc, jn, j0 == 0 ? upd : -1, j0, v, areg);
     const float w = warp_reduce<JW>(v, lane);
     if (lane < JW && j0 + lane < jn) wrow[j0 + lane] = static_cast<double>(w);
   }
@@ -263,6 +264,10 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   // (cap is a multiple of 4, so every piece below stays 16-B aligned)
   float4* la;
   float *lc, *lxh, *lx;
+  // semi: a ring of three columns of c in shared memory -- column rc of this step, rc - 1
+  // (its x-hat fold) and rc + 1, which cp.async fetches from the scratch during this step,
+  // so no pass waits on an L2 round trip (they made the CTAs' passes uneven: 7k-15k cycles)
+  float* ccol = nullptr;
   uint32_t capa = a.cap, capc = a.cap, nla = nloc;  // row strides of la / lc, samples held in la
   const uint32_t ja4 = a.ja >> 2;
   // the global scratch slice of this CTA: a_s groups [g * cap + ls]
@@ -285,9 +290,9 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       la = reinterpret_cast<float4*>(lx + a.cap);
       capa = a.nsm;
       nla = nloc < a.nsm ? nloc : a.nsm;
+      if (a.ring) ccol = reinterpret_cast<float*>(la + static_cast<uint64_t>(a.nsm) * ja4);
     }
   }
-  (void)ja4;
   float areg[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) areg[q] = 0.f;
@@ -373,6 +378,7 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
         xh = fmaf(c[r], p[r], xh);
         lc[r * capc + ls] = c[r];
       }
+      if (ccol) ccol[ls] = c[0];
       lxh[ls] = xh;
       lx[ls] = xval;
     }
@@ -394,17 +400,30 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       // fused with the xhat refresh for the previous column's step
       ulonglong2* part = a.part + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
       const uint32_t stamp = a.stamp0 + step + 1;
+      const float* c_rcn = lc + rc * capc;
+      const float* c_upd = lc + (rc ? rc - 1 : 0) * capc;
+      if (ccol) {
+        c_rcn = ccol + (rc % 3) * a.cap;
+        c_upd = ccol + ((rc + 2) % 3) * a.cap;
+        if (rc + 1 < a.P.R) {
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(ccol + ((rc + 1) % 3) * a.cap));
+          const float* src = lc + (rc + 1) * capc;
+          for (uint32_t i = tid * 4; i < nloc; i += blockDim.x * 4)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + i * 4), "l"(src + i) : "memory");
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+      }
       if constexpr (REG)
-        column_partials<32, true>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+        column_partials<32, true>(la, capa, nla, c_rcn, c_upd, lxh, lx, dbv, nloc, jn, upd, wpart + warp * a.js,
                                   lane, areg);
       else if (jn <= 8)
-        column_partials<8, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+        column_partials<8, false>(la, capa, nla, c_rcn, c_upd, lxh, lx, dbv, nloc, jn, upd, wpart + warp * a.js,
                                   lane, areg);
       else if (jn <= 16)
-        column_partials<16, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+        column_partials<16, false>(la, capa, nla, c_rcn, c_upd, lxh, lx, dbv, nloc, jn, upd, wpart + warp * a.js,
                                    lane, areg);
       else
-        column_partials<32, false>(la, capa, nla, lc, capc, lxh, lx, dbv, nloc, jn, upd, rc, wpart + warp * a.js,
+        column_partials<32, false>(la, capa, nla, c_rcn, c_upd, lxh, lx, dbv, nloc, jn, upd, wpart + warp * a.js,
                                    lane, areg);
       CORE_TRACE();  // warp partials done (warp 0)
       __syncthreads();
@@ -478,6 +497,7 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
         dbv[tid] = bnew - bold;
         bs_base[bso[n] + tid * RP + rc] = bnew;
       }
+      if (ccol) asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       CORE_TRACE();  // column stepped
       upd = static_cast<int>(rc);
@@ -564,15 +584,20 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   const char* force = std::getenv("SGDT_CORE_STATE");
   a.local = 0;
   a.nsm = 0;
+  a.ring = 1;
+  if (const char* e = std::getenv("SGDT_CORE_RING")) a.ring = std::atoi(e) != 0;
   g.reg = false;
   size_t state = stage;
   if (smem + (local > stage ? local : stage) <= kBudget && !(force && (force[0] == 'g' || force[0] == 's'))) {
     a.local = 1;
     state = local > stage ? local : stage;
   } else if (!(force && force[0] == 'g')) {
-    const size_t fixed = smem + 2 * static_cast<size_t>(a.cap) * sizeof(float);
-    if (fixed < kBudget) {
-      uint64_t nsm = ((kBudget - fixed) / (a.ja * sizeof(float))) & ~uint64_t(3);
+    // xhat, x and the three-column ring of c; the semi state may use all but a margin of the
+    // 227 KB an SM offers one CTA
+    constexpr size_t kSemiBudget = 216 * 1024;
+    const size_t fixed = smem + 5 * static_cast<size_t>(a.cap) * sizeof(float);
+    if (fixed < kSemiBudget) {
+      uint64_t nsm = ((kSemiBudget - fixed) / (a.ja * sizeof(float))) & ~uint64_t(3);
       if (const char* e = std::getenv("SGDT_CORE_NSM")) {  // tests: force register-resident samples
         const uint64_t lim = std::strtoull(e, nullptr, 10);
         if (lim >= 1 && lim < nsm) nsm = (lim + 3) & ~uint64_t(3);
@@ -587,7 +612,7 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
       if (nsm) {
         a.local = 2;
         a.nsm = static_cast<uint32_t>(nsm);
-        const size_t semi = (2 * static_cast<size_t>(a.cap) + nsm * a.ja) * sizeof(float);
+        const size_t semi = (5 * static_cast<size_t>(a.cap) + nsm * a.ja) * sizeof(float);
         state = semi > stage ? semi : stage;
       }
     }

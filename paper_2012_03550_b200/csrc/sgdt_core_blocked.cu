@@ -131,6 +131,7 @@ struct BlockedArgs {
   double* part;  // grid x kstride
   unsigned* ticket;
   uint32_t st;   // samples per smem tile
+  int q_mask;    // final step: bit k = refresh Q^(k) here (the other modes: tensor-core refresh)
 };
 
 // Replay the T column steps of a block from its summed vector v (smem):
@@ -401,7 +402,8 @@ __global__ void __launch_bounds__(kBlk) core_block_kernel(BlockedArgs a) {
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + warp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * nwarps;
     for (int k = 0; k < a.P.order; ++k)
-      q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs + bso[k], a.P.dims[k], gw, nw, stage, lane);
+      if (a.q_mask >> k & 1)
+        q_rows_tiled<RP>(a.P.A[k], a.P.Q[k], a.P.J[k], bs + bso[k], a.P.dims[k], gw, nw, stage, lane);
   }
 
   // ---- two-level ticket reduction (no CTA waits): the last CTA of each group
@@ -603,14 +605,26 @@ int launch_core_block_step(Session& s, uint32_t k) {
   a.part = s.core_part;
   a.ticket = s.core_ticket;
   a.st = pl.st;
+  // final step: wide modes with many rows are refreshed by the tensor-core kernel
+  // after this one (it reads the B this step's last CTA writes), as in launch_core
+  int tc_modes = 0;
+  if (a.n < 0)
+    for (int q = 0; q < s.order; ++q)
+      if (q_refresh_tc_eligible(s, q)) tc_modes |= 1 << q;
+  a.q_mask = ((1 << s.order) - 1) & ~tc_modes;
+  int rc = SGDT_ERR_CONFIG;
   switch (s.RP) {
 #define BL(RP) \
-  case RP: return blocked_launch_rp<RP>(s, a, pl.grid, pl.smem);
+  case RP: rc = blocked_launch_rp<RP>(s, a, pl.grid, pl.smem); break;
     BL(4) BL(8) BL(12) BL(16) BL(20) BL(24) BL(28) BL(32)
 #undef BL
-    default: break;
+    default: return fail(SGDT_ERR_CONFIG, "unsupported R_core");
   }
-  return fail(SGDT_ERR_CONFIG, "unsupported R_core");
+  if (rc != SGDT_OK) return rc;
+  for (int q = 0; q < s.order; ++q)
+    if (tc_modes >> q & 1)
+      if (int r2 = launch_q_refresh_tc(s, q)) return r2;
+  return SGDT_OK;
 }
 
 // Fill the launch geometry of a plan whose T, m, lo, hi are set.

@@ -149,3 +149,28 @@ def test_core_semi_local_state_matches_oracle(monkeypatch, J, R, nsm):
             assert np.array_equal(out["semi"][n], out["global"][n]), f"B^({n}): semi vs global state"
         else:
             assert rel_err(out["semi"][n], out["global"][n]) <= 1e-6, f"B^({n}): semi vs global state"
+
+
+def test_blocked_core_uses_tensor_core_refresh(monkeypatch):
+    """The blocked (multi-GPU) core phase hands wide modes to the same refresh kernel."""
+    monkeypatch.setenv("SGDT_QTC", "1")
+    monkeypatch.setenv("SGDT_CORE", "blocked")
+    dims, J, R, nnz, bm = (300, 200, 130), (32, 32, 32), 32, 15000, 400
+    sig = unit_sigma(dims, J, R)
+    tr, _ = make_case(dims, J, 16, nnz, 17, tm=0.0, ts=sig)
+    t = O.Tensor(dims, *tr)
+    s = session_for(dims, tr, J, R)
+    m = oracle_model(dims, J, R, 23, sd=sig, mean=0.0)
+    rng = O.Rng(5)
+    ws = O.CoreWorkspace(nnz)
+    s.set_rng(*rng.state())
+    s.set_model(*m.params())
+    s.core_epoch(0.01, 0.01, bm)
+    O.update_core_epoch(m, t, 0.01, 0.01, bm, rng, ws)
+    Ad, Bd = s.get_model()
+    _, RB = m.params()
+    for n in range(3):
+        assert rel_err(Bd[n], RB[n]) <= TOL, f"core B^({n})"
+        ref, mag = host_q(Ad[n], Bd[n])
+        err = np.max(np.abs(s.q_rows(n).astype(np.float64) - ref) / np.maximum(mag, 1e-30))
+        assert err <= 1e-6, f"Q^({n}) after the blocked core phase: {err}"
