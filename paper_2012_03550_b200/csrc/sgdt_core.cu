@@ -66,16 +66,18 @@ struct CoreArgs {
   float* sxh;         // m           xhat_s
   float* sx;          // m           x_s
   ulonglong2* part;   // 2 x js x grid stamped partials
-  unsigned long long* res;  // 2 x js stamped new column values
+  unsigned long long* res;  // 2 x grid x js stamped new column values, one copy per CTA
   uint32_t stamp0;    // stamps of this launch are stamp0 + step + 1
   int grid_sync;      // exchange through grid.sync() instead of the stamps (A/B)
-  long long* trace;   // SGDT_CORE_TRACE: clock64() of CTA 0 at the phase boundaries
+  long long* trace;   // SGDT_CORE_TRACE: clock64() of CTA trace_cta at the phase boundaries
+  int trace_cta;      // SGDT_CORE_TRACE_CTA (default 0)
   double lr, reg;
   int* flag;
   int q_refresh;      // bit k: fuse Q^(k) = A^(k) B^(k) at the end (the other modes go to the tensor-core refresh)
   int local;          // per-sample state of the CTA's slice: 1 shared memory, 0 global scratch, 2 semi
                       // (a_s in shared memory / registers, xhat and x in shared memory, c_{s,r} global)
   uint32_t cap;       // samples per CTA slice (upper bound)
+  int res_copies;     // the new column goes to one word per CTA (wide J) instead of one shared word
   int ring;           // semi: keep a three-column ring of c in shared memory (SGDT_CORE_RING=0: A/B)
   uint32_t nsm;       // semi: samples whose a_s sit in shared memory (row stride nsm); the samples
                       // nsm + t, t < blockDim, keep a_s in the registers of thread t
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
   int ti = 0;
 #define CORE_TRACE()                                                    \
   do {                                                                  \
-    if (a.trace && blockIdx.x == 0 && tid == 0 && ti < kCoreTraceCap) a.trace[ti++] = clock64(); \
+    if (a.trace && blockIdx.x == a.trace_cta && tid == 0 && ti < kCoreTraceCap) a.trace[ti++] = clock64(); \
   } while (0)
   CORE_TRACE();
   for (int k = 0; k < a.P.order; ++k)
@@ -438,7 +440,12 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       // ---- reducers: column j of V belongs to one warp of the grid (CTA j % grid).  It
       // sums the CTA partials in CTA order (fixed lane striding + butterfly), takes the
       // sgd_step on b_{j,rc} and publishes the new value
-      unsigned long long* res = a.res + static_cast<uint64_t>(step & 1) * a.js;
+      // wide J: every CTA polls its own copy of the new column.  148 CTAs polling the same
+      // lines serialise at their L2 slice (J = 32: store -> all-see ~6k cycles against ~1.5k
+      // for a line with one reader), so the reducer stores one word per CTA; with J < 16 the
+      // shared words are faster (config 2 core 0.163 vs 0.175 ms, config 3 0.364 vs 0.374)
+      unsigned long long* res = a.res + static_cast<uint64_t>(step & 1) * gridDim.x * a.js;
+      const uint64_t res_stride = a.res_copies ? a.js : 0;
       for (uint32_t j = blockIdx.x + warp * gridDim.x; j < jn; j += nwarps * gridDim.x) {
         const ulonglong2* pj = part + static_cast<uint64_t>(j) * gridDim.x;
         double V = 0.0;
@@ -467,22 +474,23 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
             if (b0 + q * 32 + lane < gridDim.x)
               V += __longlong_as_double(static_cast<long long>((w[q].y << 32) | (w[q].x & 0xffffffffull)));
         }
-        if (a.trace && blockIdx.x == 0 && tid == 0 && ti < kCoreTraceCap) {
+        if (a.trace && blockIdx.x == a.trace_cta && tid == 0 && ti < kCoreTraceCap) {
           a.trace[kCoreTraceCap + ti] = rounds;
           a.trace[ti++] = clock64();  // partials polled
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) V += __shfl_xor_sync(0xffffffffu, V, o);
-        if (lane == 0) {
+        {  // every lane forms the same step (V is the warp-wide sum in all lanes)
           double w = static_cast<double>(bs_base[bso[n] + j * RP + rc]);
           int bad = (!isfinite(w) ? 1 : 0) | (!isfinite(V) ? 2 : 0);
           w -= a.lr * (V * inv_m + a.reg * w);
           const float bnew = static_cast<float>(w);
           bad |= !isfinite(bnew) ? 4 : 0;
-          if (bad) atomicOr(a.flag, bad);
+          if (bad && lane == 0) atomicOr(a.flag, bad);
           const unsigned long long word =
               (static_cast<unsigned long long>(stamp) << 32) | static_cast<unsigned long long>(__float_as_uint(bnew));
-          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(res + j), "l"(word) : "memory");
+          for (unsigned c = lane; c < (a.res_copies ? gridDim.x : 1u); c += 32)
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(res + c * res_stride + j), "l"(word) : "memory");
         }
       }
       CORE_TRACE();  // reducer role done
@@ -490,7 +498,10 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       if (tid < static_cast<int>(jn)) {
         unsigned long long word;
         do {
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(word) : "l"(res + tid) : "memory");
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];"
+                       : "=l"(word)
+                       : "l"(res + blockIdx.x * res_stride + tid)
+                       : "memory");
         } while (static_cast<uint32_t>(word >> 32) != stamp);
         const float bnew = __uint_as_float(static_cast<uint32_t>(word));
         const float bold = bs_base[bso[n] + tid * RP + rc];
@@ -586,6 +597,8 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   a.nsm = 0;
   a.ring = 1;
   if (const char* e = std::getenv("SGDT_CORE_RING")) a.ring = std::atoi(e) != 0;
+  a.res_copies = a.js >= 16;  // config 4 (J = 16): 0.463 -> 0.451 ms, config 5 (J = 32): 2.17 -> 1.96 ms
+  if (const char* e = std::getenv("SGDT_CORE_RES")) a.res_copies = e[0] == 'p';  // percta | shared (A/B)
   g.reg = false;
   size_t state = stage;
   if (smem + (local > stage ? local : stage) <= kBudget && !(force && (force[0] == 'g' || force[0] == 's'))) {
@@ -644,6 +657,8 @@ int core_launch_rp(Session& s, CoreArgs& a, size_t smem) {
   const bool trace = std::getenv("SGDT_CORE_TRACE") && traced < 4;
   if (trace && !d_trace) SGDT_CUDA(cudaMalloc(&d_trace, 2 * kCoreTraceCap * sizeof(long long)));
   a.trace = trace ? d_trace : nullptr;
+  a.trace_cta = 0;
+  if (const char* e = std::getenv("SGDT_CORE_TRACE_CTA")) a.trace_cta = std::atoi(e) % grid;
   if (trace) SGDT_CUDA(cudaMemsetAsync(d_trace, 0, 2 * kCoreTraceCap * sizeof(long long), s.stream));
   void* args[] = {&a};
   SGDT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(block),
@@ -707,7 +722,7 @@ int launch_core(Session& s, const sgdt_core_hyper& h, const uint32_t* batches, u
     // the slots are cleared so that no stale stamp can match
     const uint32_t steps = static_cast<uint32_t>(s.order) * s.R;
     if (s.core_stamp > 0xffffffffu - steps - 1) {
-      SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 2ull * (s.num_sms + 1) * js * sizeof(ulonglong2), s.stream));
+      SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 3ull * s.num_sms * js * sizeof(ulonglong2), s.stream));
       s.core_stamp = 0;
     }
     a.stamp0 = s.core_stamp;

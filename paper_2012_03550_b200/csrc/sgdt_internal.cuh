@@ -219,7 +219,7 @@ struct Session {
   float* cs_c = nullptr;      // M x R
   float* cs_xhat = nullptr;   // M
   float* cs_x = nullptr;      // M
-  ulonglong2* cs_part = nullptr;  // 2 x Jmax x grid stamped partials (sgdt_core.cu)
+  ulonglong2* cs_part = nullptr;  // 2 x Jmax x grid stamped partials + per-CTA new-column words (sgdt_core.cu)
   uint32_t core_stamp = 0;        // last stamp used in cs_part
   uint64_t cs_cap = 0;
   int core_grid = 0, core_block = 0;

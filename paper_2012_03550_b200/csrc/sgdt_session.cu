@@ -744,8 +744,9 @@ int ensure_core_capacity(Session& s, uint64_t m) {
   TRY(dalloc(&s.cs_c, mm * s.RP));
   TRY(dalloc(&s.cs_xhat, mm));
   TRY(dalloc(&s.cs_x, mm));
-  TRY(dalloc(&s.cs_part, 2ull * (s.num_sms + 1) * js));  // + the new-column words
-  SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 2ull * (s.num_sms + 1) * js * sizeof(ulonglong2), s.stream));
+  // stamped partials (2 x js x grid) + every CTA's own copy of the new-column words (2 x grid x js u64)
+  TRY(dalloc(&s.cs_part, 3ull * s.num_sms * js));
+  SGDT_CUDA(cudaMemsetAsync(s.cs_part, 0, 3ull * s.num_sms * js * sizeof(ulonglong2), s.stream));
   s.core_stamp = 0;
   s.cs_cap = m;
   return SGDT_OK;
