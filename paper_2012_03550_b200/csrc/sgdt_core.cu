@@ -77,6 +77,7 @@ struct CoreArgs {
   int local;          // per-sample state of the CTA's slice: 1 shared memory, 0 global scratch, 2 semi
                       // (a_s in shared memory / registers, xhat and x in shared memory, c_{s,r} global)
   uint32_t cap;       // samples per CTA slice (upper bound)
+  int q_rows;         // gather the current Q^(k) rows (k > n, and the own mode's) instead of forming a^(k) B^(k)
   int res_copies;     // the new column goes to one word per CTA (wide J) instead of one shared word
   int ring;           // semi: keep a three-column ring of c in shared memory (SGDT_CORE_RING=0: A/B)
   uint32_t nsm;       // semi: samples whose a_s sit in shared memory (row stride nsm); the samples
@@ -335,6 +336,18 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
           in_ = ikk;
           continue;
         }
+        if (a.q_rows && k > n) {
+          // B^(k) has not been stepped yet in this phase, so the device's Q^(k) row
+          // (refreshed after the last core phase, rewritten by the factor finalisers)
+          // is a^(k) B^(k): one row gather instead of a J x R contraction
+          const float4* qrow = reinterpret_cast<const float4*>(a.P.Q[k] + static_cast<uint64_t>(ikk) * RP);
+#pragma unroll
+          for (int r4 = 0; r4 < RP / 4; ++r4) {
+            const float4 q = __ldg(qrow + r4);
+            c[4 * r4] *= q.x, c[4 * r4 + 1] *= q.y, c[4 * r4 + 2] *= q.z, c[4 * r4 + 3] *= q.w;
+          }
+          continue;
+        }
         const float* arow = a.P.A[k] + static_cast<uint64_t>(ikk) * a.P.J[k];
         float d[RP];
 #pragma unroll
@@ -356,8 +369,17 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
       }
       const float* arow = a.P.A[n] + static_cast<uint64_t>(in_) * jn;
       float p[RP];
+      if (a.q_rows) {  // the own mode's row of Q^(n) is a_s B^(n) at the start of the mode
+        const float4* qrow = reinterpret_cast<const float4*>(a.P.Q[n] + static_cast<uint64_t>(in_) * RP);
 #pragma unroll
-      for (int r = 0; r < RP; ++r) p[r] = 0.f;
+        for (int r4 = 0; r4 < RP / 4; ++r4) {
+          const float4 q = __ldg(qrow + r4);
+          p[4 * r4] = q.x, p[4 * r4 + 1] = q.y, p[4 * r4 + 2] = q.z, p[4 * r4 + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) p[r] = 0.f;
+      }
       for (uint32_t j0 = 0; j0 < jn; j0 += 8) {
         float av[8];
         load_row8(arow, j0, jn, av);
@@ -367,12 +389,14 @@ __global__ void __launch_bounds__(kCoreBlock) core_kernel(CoreArgs a) {
           dst[0] = make_float4(av[0], av[1], av[2], av[3]);
           if (j0 + 4 < jn) dst[dstride] = make_float4(av[4], av[5], av[6], av[7]);
         }
+        if (!a.q_rows) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (j0 + q < jn) {
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q < jn) {
 #pragma unroll
-            for (int r = 0; r < RP; ++r) p[r] = fmaf(av[q], bs_base[bso[n] + (j0 + q) * RP + r], p[r]);
-          }
+              for (int r = 0; r < RP; ++r) p[r] = fmaf(av[q], bs_base[bso[n] + (j0 + q) * RP + r], p[r]);
+            }
+        }
       }
       float xh = 0.f;
 #pragma unroll
@@ -597,6 +621,10 @@ int core_geometry(Session& s, CoreArgs& a, CoreGeom& g) {
   a.nsm = 0;
   a.ring = 1;
   if (const char* e = std::getenv("SGDT_CORE_RING")) a.ring = std::atoi(e) != 0;
+  // Q row gathers in the sample setup: every Q^(k) is current when a core phase starts
+  // (set_model, the last core phase's refresh, the factor finalisers); SGDT_CORE_QROWS=0: A/B
+  a.q_rows = 1;
+  if (const char* e = std::getenv("SGDT_CORE_QROWS")) a.q_rows = std::atoi(e) != 0;
   a.res_copies = a.js >= 16;  // config 4 (J = 16): 0.463 -> 0.451 ms, config 5 (J = 32): 2.17 -> 1.96 ms
   if (const char* e = std::getenv("SGDT_CORE_RES")) a.res_copies = e[0] == 'p';  // percta | shared (A/B)
   g.reg = false;

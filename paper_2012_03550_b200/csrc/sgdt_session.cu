@@ -1672,10 +1672,9 @@ int sgdt_run_epochs_host(sgdt_session* s, const sgdt_core_hyper* ch, const sgdt_
     SGDT_CUDA(cudaGetLastError());
     s->launches += 2;
   }
-  // Q^(k) = A^(k) B^(k): the core kernel reads only A and B and rewrites every
-  // Q^(k) at its tail, so the refresh is needed only when no core phase runs
-  if (epochs == 0 || !(ch->lr > 0.0))
-    for (int k = 0; k < s->order; ++k) TRY(launch_q_refresh(*s, k));
+  // Q^(k) = A^(k) B^(k) for the model just copied in: the factor phase gathers Q rows,
+  // and so does the core phase's sample setup (sgdt_core.cu)
+  for (int k = 0; k < s->order; ++k) TRY(launch_q_refresh(*s, k));
   if (epochs == 0) {
     SGDT_CUDA(cudaStreamSynchronize(s->stream));
     return sgdt_get_model(s, A_out, B_out);
