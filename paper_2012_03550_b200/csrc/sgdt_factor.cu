@@ -655,8 +655,15 @@ __device__ __forceinline__ void group_row(const float4& v, int grp, int gi, int 
   __syncwarp();
 }
 
-template <int RP, int NO>
-__global__ void __launch_bounds__(256, 4) factor_group_kernel(FactorArgs a) {
+// MINB: resident CTAs per SM the register budget is cut for.  4 (64 registers) is the
+// default.  5 (51 registers, 40 warps per SM) is used for 3-order tensors when every
+// gathered Q table is far larger than the L2, i.e. the mode waits on DRAM row gathers and
+// more warps in flight pay: config 5 mode 2 (two 1.28 GB tables) 7.26 -> 6.73 ms; with a
+// small table among them it is slower (config 5 modes 0/1 10.25 -> 10.6 ms), and with
+// more gathered rows per entry it spills (config 4, N = 5: 0.98 -> 1.65 ms per mode);
+// 6 CTAs per SM (42 registers) spill as well (config 5: 10.2 -> 16.0 ms per mode).
+template <int RP, int NO, int MINB>
+__global__ void __launch_bounds__(256, MINB) factor_group_kernel(FactorArgs a) {
   constexpr int G = Lanes<RP>::G, E = Lanes<RP>::E;
   __shared__ __align__(16) float bsn[SGDT_MAX_J * bstride<RP>()];
   __shared__ __align__(16) float wscr[8 * kWarpScratch];
@@ -961,8 +968,25 @@ int factor_launch(Session& s, FactorArgs& a) {
       return e && atoi(e) != 0;
     }();
     const int sj = RP >= 16 || force_group ? -1 : staged_table<RP, NO>(a);
-    if (RP >= 16 || force_group)
-      factor_group_kernel<RP, NO><<<grid, block, 0, s.stream>>>(a);
+    if (RP >= 16 || force_group) {
+      bool dram_bound = NO == 2;  // every gathered table > 64 MB (half the L2)
+      for (int k = 0; k < s.order; ++k)
+        if (k != a.n && static_cast<uint64_t>(s.dims[k]) * RP * sizeof(float) <= (64ull << 20)) dram_bound = false;
+      static const int minb_env = [] {  // SGDT_GROUP_MINB=4|5 forces a variant (A/B runs)
+        const char* e = getenv("SGDT_GROUP_MINB");
+        return e ? atoi(e) : 0;
+      }();
+      if (minb_env == 4) dram_bound = false;
+      if (minb_env == 5) dram_bound = NO == 2;
+      if constexpr (NO == 2) {
+        if (dram_bound)
+          factor_group_kernel<RP, NO, 5><<<grid, block, 0, s.stream>>>(a);
+        else
+          factor_group_kernel<RP, NO, 4><<<grid, block, 0, s.stream>>>(a);
+      } else {
+        factor_group_kernel<RP, NO, 4><<<grid, block, 0, s.stream>>>(a);
+      }
+    }
     else {
       // T2 (half-width tail loads) is instantiated for RP = 12 only (R = 9, 10)
       static const bool t2_off = [] {  // SGDT_T2=0: full-width tails (A/B runs)
