@@ -1,5 +1,6 @@
 // sgdt_core.cu -- K2/K3/K4: the core (Kruskal B^(n)) phase as one cooperative
-// kernel, plus the Q^(k) = A^(k) B^(k) refresh fused at its tail.
+// kernel, plus the Q^(k) = A^(k) B^(k) refresh fused at its tail (wide modes with many
+// rows go to the tensor-core refresh of sgdt_qrefresh_tc.cu, launched right after).
 //
 // Reference: update_core_epoch (core_optimizer.cpp:112-257).  For each mode n
 // (ascending) and each r_core (ascending, Gauss-Seidel over the columns):
@@ -13,10 +14,18 @@
 // after every column update (xhat_s += c_{s,rc} a_s . delta_b).
 //
 // Each CTA owns the contiguous sample slice partition_even(M, grid)[cta]
-// (scheduler.cpp:34-46).  A step's partial V goes to a double-buffered global
+// (scheduler.cpp:34-46).  Its per-sample state (a_s in float4 groups, c_{s,r},
+// xhat_s, x_s) lives in shared memory when it fits; otherwise a_s stays in shared
+// memory plus one register-resident sample per thread, xhat / x in shared memory
+// and c in an L2-resident scratch with a three-column cp.async ring (core_geometry).
+// The setup of a mode gathers the device's current Q^(k) rows for the modes whose
+// B^(k) has not been stepped yet in this phase (k > n) and for x-hat the own mode's
+// row; only the modes already stepped need a^(k) B^(k) from the shared-memory B.
+// A step's partial V goes to a double-buffered global
 // array; column j of V belongs to one reducer warp of the grid (CTA j % grid),
 // which sums the CTA partials in CTA order (fp64), takes the sgd_step on
-// b_{j,rc} and publishes the new value; every CTA then installs the identical
+// b_{j,rc} and publishes the new value (one shared word, or for J >= 16 one word
+// per CTA so that no line is polled by every SM); every CTA then installs the identical
 // column in its shared-memory copy of B.  One exchange per (n, r_core).
 //
 // The exchange carries its own arrival flags: a partial (one double) is stored
