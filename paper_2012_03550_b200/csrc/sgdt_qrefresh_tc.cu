@@ -299,14 +299,11 @@ int launch_q_refresh_tc(Session& s, int k) {
   if (int rc = make_row_tile_map(&map_q, s.P.Q[k], s.dims[k])) return rc;
   const uint32_t tiles = (s.dims[k] + kTileRows - 1) / kTileRows;
   const size_t smem = sizeof(QTcSmem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    SGDT_CUDA(cudaFuncSetAttribute(q_refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    SGDT_CUDA(cudaFuncSetAttribute(q_refresh_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   cudaSharedmemCarveoutMaxShared));
-    attr = true;
-  }
+  // per device (a process may drive several), cheap host calls
+  SGDT_CUDA(cudaFuncSetAttribute(q_refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  SGDT_CUDA(cudaFuncSetAttribute(q_refresh_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
   // resident CTAs per SM by shared memory (227 KB per SM, 1 KB reserved per CTA; 32 TMEM
   // columns and 64 registers x 128 threads per CTA are far from their limits)
   int per_sm = static_cast<int>((227u * 1024u) / (smem + 1024u));
